@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark: whole-frame encode + decode throughput of the integer-only octree coder.
+
+Workload (BASELINE.json configs[1], "cfg2"): synthetic KITTI-shaped 64-beam x
+2048-azimuth frames (~131k points, ~56k voxels), 12-level octree, full GRED+XFP model
+(C = H = 32, seeded random int8 weights).  One step = encode B frames (device int32
+xyz -> device bitstreams) + decode them (device bitstreams -> device xyz): every row of
+SURVEY.md §8(a).  Frames shard by index across ranks (weak scaling, no data-path
+collective); NCCL only gathers per-rank stats.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "enc/dec frames/s at 1/2/4/8 B200; bit-exact bitstream vs CPU oracle; bpp"
+UNIT = "frames/s"
+WORKLOAD = "cfg2: KITTI-shaped 64x2048 LiDAR frames (synthetic ray-cast), L=12, C=H=32 GRED+XFP int8 model"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_inputs(cfg, B: int, first: int):
+    from paper_2603_25260_b200 import inputs as I
+    frames = I.make_frames(cfg, B, first=first, scene_seed=1)
+    offs = np.cumsum([0] + [len(f) for f in frames]).tolist()
+    return frames, offs
+
+
+# --------------------------------------------------------------------------------------
+# reference arm: the CPU oracle as it stands (BASELINE tier framing: the oracle is the
+# reference arm), run on host cores, rank 0 only.
+# --------------------------------------------------------------------------------------
+
+def oracle_rate(frames, L, model_bytes, threads: int):
+    """Encode+decode each frame with the oracle; returns (frames/s, seconds, cores used)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import oracle as O
+    m = O.Model(model_bytes)
+
+    def one(f):
+        bs = O.encode(m, f, L)
+        O.decode(m, bs)
+        return len(bs)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(one, frames))
+    dt = time.perf_counter() - t0
+    return len(frames) / dt, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2603_25260_b200 import inputs as I
+    cfg = I.CFG2
+    mb = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18).to_bytes()
+    cores = max(1, min(os.cpu_count() or 1, 8))
+    frames, _ = make_inputs(cfg, cores, 0)
+    for _ in range(args.warmup):
+        oracle_rate(frames[:1], cfg.bit_depth, mb, 1)
+    ts = []
+    for _ in range(args.steps):
+        _, dt = oracle_rate(frames, cfg.bit_depth, mb, cores)
+        ts.append(dt)
+    tot = sum(ts)
+    value = cores * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64 (scalar CPU)",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "frames_per_step": cores},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{cores} cfg2 frames per step (encode+decode), one frame per thread"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------
+
+ALU_PEAK_NOTE = ("B200 integer issue peak = 148 SM x 4 SMSP x 32 lanes x 1 instr/clk x sm_max clock "
+                 "(DESIGN.md §5)")
+
+
+def run_ours(args, rank, world, dist):
+    import torch
+    from paper_2603_25260_b200 import inputs as I
+    from paper_2603_25260_b200 import pcc
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(dev)
+    cfg = I.CFG2
+    L = cfg.bit_depth
+    B = args.batch
+    mb = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18).to_bytes()
+    frames, offs = make_inputs(cfg, B, rank * B)
+    npts = offs[-1]
+    host_xyz = torch.from_numpy(np.concatenate(frames).astype(np.int32)).pin_memory()
+    codec = pcc.Codec(mb, dev, stream)
+    with torch.cuda.stream(stream):
+        d_xyz = host_xyz.to(f"cuda:{dev}", non_blocking=True)
+        cap = sum(pcc.pcc_encode_bound(offs[i + 1] - offs[i], L) + 4 for i in range(B))
+        d_bs = torch.empty(cap, dtype=torch.uint8, device=f"cuda:{dev}")
+        d_out = torch.empty((npts, 3), dtype=torch.int32, device=f"cuda:{dev}")
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    stream.synchronize()
+
+    def step(evs=None):
+        if evs:
+            evs[0].record(stream)
+        oo = pcc.pcc_encode_batch(codec.ctx, codec.model, d_xyz, offs, L, d_bs, cap)
+        if evs:
+            evs[1].record(stream)
+        no = pcc.pcc_decode_batch(codec.ctx, codec.model, d_bs, oo, d_out, npts)
+        if evs:
+            evs[2].record(stream)
+        return oo, no
+
+    for _ in range(args.warmup):
+        oo, no = step()
+    stream.synchronize()
+    nvox = no[-1]
+    nbytes = oo[-1]
+
+    # parity sample (outside the timed region): frame 0 vs the CPU oracle, and round trip
+    parity = None
+    if not args.no_parity and rank == 0:
+        from oracle import oracle as O
+        got = d_bs[oo[0]:oo[1]].cpu().numpy().tobytes()
+        want = O.encode(O.Model(mb), frames[0], L)
+        dec = d_out[no[0]:no[1]].cpu().numpy()
+        ref, _ = O.decode(O.Model(mb), want)
+        parity = bool(got == want and np.array_equal(dec, ref))
+
+    # ---- timed region: K steps, L2 flushed between steps (outside the events) ----
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with Clocks(dev) as clk:
+        t_wall0 = time.perf_counter()
+        for k in range(K):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            oo, no = step(evs[k])
+        stream.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
+    dec_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
+    tot_ms = enc_ms + dec_ms
+
+    # own-kernel launches per step: count one encode and one decode separately
+    pcc.pcc_encode_batch(codec.ctx, codec.model, d_xyz, offs, L, d_bs, cap)
+    enc_l = pcc.pcc_ctx_launch_count(codec.ctx)
+    pcc.pcc_decode_batch(codec.ctx, codec.model, d_bs, oo, d_out, npts)
+    dec_l = pcc.pcc_ctx_launch_count(codec.ctx)
+    gpu_launches = K * (enc_l + dec_l)
+
+    # ---- profiled pass (CUDA events around every launch, same stream) ----
+    pcc.pcc_ctx_set_profile(codec.ctx, True)
+    KP = max(1, min(K, 5))
+    for _ in range(KP):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        step()
+    prof = {}
+    for cname in pcc.pcc_ctx_profile_categories(codec.ctx):
+        ms, nl, nb = pcc.pcc_ctx_profile_get(codec.ctx, cname)
+        prof[cname] = {"ms_per_step": ms / KP, "launches_per_step": nl / KP, "bytes_per_step": nb / KP}
+    pcc.pcc_ctx_set_profile(codec.ctx, False)
+    prof_total = sum(v["ms_per_step"] for v in prof.values())
+
+    # ---- e2e through the host-buffer C ABI (H2D inputs + D2H results inside) ----
+    h_bs = torch.empty(cap, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty((npts, 3), dtype=torch.int32).pin_memory()
+    KE = max(1, min(K, 5))
+    e2e_ms = 0.0
+    h2d = d2h = 0
+    for k in range(KE + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        oo_h = pcc.pcc_encode_batch_host(codec.ctx, codec.model, host_xyz, offs, L, h_bs, cap)
+        no_h = pcc.pcc_decode_batch_host(codec.ctx, codec.model, h_bs, oo_h, h_out, npts)
+        e1.record(stream)
+        stream.synchronize()
+        if k > 0:  # first is a warm-up of the e2e buffers
+            e2e_ms += e0.elapsed_time(e1)
+        h2d = npts * 12 + oo_h[-1]
+        d2h = oo_h[-1] + no_h[-1] * 12
+    e2e_ms /= KE
+
+    # coded symbols per step (levels R..L-1 of every frame), for per-node op counts
+    coded_per_step = 0
+    for i in range(B):
+        cnt = pcc.pcc_build_octree(codec.ctx, d_xyz[offs[i]:offs[i + 1]], offs[i + 1] - offs[i], L)
+        coded_per_step += sum(cnt[4:L])
+
+    # ---- gather per-rank stats (the only collective) ----
+    stats = np.array([B, npts, nvox, nbytes, int(enc_ms * 1e6), int(dec_ms * 1e6), int(parity is False),
+                      int(tot_ms * 1e6)], np.int64)
+    if dist:
+        t = torch.from_numpy(stats).to(f"cuda:{dev}")
+        allst = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(allst, t)
+        allst = np.stack([a.cpu().numpy() for a in allst])
+        e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e_ms_max = float(e2e_t.item())
+    else:
+        allst = stats[None]
+        e2e_ms_max = e2e_ms
+    if rank != 0:
+        return
+    frames_tot = int(allst[:, 0].sum()) * K
+    t_max_ms = float(allst[:, 7].max()) / 1e6
+    value = frames_tot / (t_max_ms / 1e3)
+    enc_fps = frames_tot / (float(allst[:, 4].max()) / 1e9)
+    dec_fps = frames_tot / (float(allst[:, 5].max()) / 1e9)
+    pts_tot = int(allst[:, 1].sum()) * K
+
+    # ---- roofline of the dominant kernel category ----
+    pk, pk_src = peaks()
+    top = max(prof.items(), key=lambda kv: kv[1]["ms_per_step"]) if prof else (None, None)
+    roof = None
+    if top[0]:
+        name, v = top
+        sm_max = float(pk.get("sm_max_mhz", 1965.0))
+        if name in ("head_enc", "head_dec", "rans_enc", "rans_dec"):
+            # ALU-bound: algorithmic integer ops per node
+            C = H = 32
+            ops_per_node = {"head_enc": (C * H + H * 255) / 4 + 255 * 8,
+                            "head_dec": (C * H + H * 255) / 4 + 255 * 9,
+                            "rans_enc": 30, "rans_dec": 40}[name]
+            coded_nodes = coded_per_step
+            achieved = coded_nodes * ops_per_node / (v["ms_per_step"] / 1e3) / 1e12
+            peak = 148 * 4 * 32 * sm_max * 1e6 / 1e12
+            roof = {"kernel": name, "bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
+                    "frac": achieved / peak, "traffic": None, "peak_src": ALU_PEAK_NOTE,
+                    "share_of_step": v["ms_per_step"] / prof_total}
+        else:
+            achieved = v["bytes_per_step"] / (v["ms_per_step"] / 1e3) / 1e9
+            peak = float(pk["hbm_gbs"])
+            roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None, "peak_src": pk_src,
+                    "share_of_step": v["ms_per_step"] / prof_total}
+
+    # ---- CPU baseline: the oracle on a bounded sample of the same workload ----
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cores = max(1, min(os.cpu_count() or 1, 4))
+        rate, dt = oracle_rate(frames[:cores], L, mb, cores)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{cores} cfg2 frames encode+decode, one thread per frame ({dt:.1f} s)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": t_max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int8 x int8 -> int32 (integer-only)", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "frames_per_gpu_per_step": B, "global_batch": B * world,
+                   "points_per_frame": npts / B, "voxels_per_frame": nvox / B, "parallelism": f"frames/dp{world}",
+                   "l2": "flushed between steps (256 MiB write, outside the events)"},
+        "enc_fps": enc_fps, "dec_fps": dec_fps, "points_per_s": pts_tot / (t_max_ms / 1e3),
+        "bpp": 8.0 * nbytes / npts, "bits_per_voxel": 8.0 * nbytes / nvox,
+        "parity_sample_frame0": parity, "wall_s_timed_region": t_wall,
+        "gpu_launches": gpu_launches,
+        "e2e": {"value": B * world / (e2e_ms_max / 1e3) if e2e_ms_max else None, "unit": UNIT,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "clocks": clk.summary(),
+        "roofline": roof,
+        "profile_ms_per_step": {k: round(v["ms_per_step"], 4) for k, v in sorted(prof.items())},
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as D
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        D.init_process_group("nccl")
+        dist = D
+    run_ours(args, rank, world, dist)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,141 @@
+/*
+ * pcc.h — C ABI of the B200-native integer-only octree LiDAR coder.
+ *
+ * Hot path of "Towards Practical Lossless Neural Compression for LiDAR Point
+ * Clouds" (arxiv 2603.25260; PAPER.md = P:<line>).  Per octree level the coder
+ * builds the Morton-ordered voxel set and its occupancy bytes, runs
+ * the GRED / XFP context network in integer-only arithmetic (Eq.4-14),
+ * turns the predictor's 255 logits into an exact Q16 distribution with a LUT
+ * softmax (Eq.15) and rANS-codes the occupancy bytes (
+ * the coder itself is our reading Q23).  Decoding is level-serial
+ * (Eq.2) and parallel within a level.
+ *
+ * Conventions (all functions):
+ *  - Every compute call requires an sm_100 device; there is no CPU fallback.
+ *    Without one, calls return PCC_ERR_CUDA.
+ *  - Buffers named d_* are DEVICE pointers owned by the caller (e.g. torch tensors'
+ *    data_ptr()); h_* and plain arrays are HOST pointers owned by the caller.  The
+ *    library never frees caller memory.  Handles (pcc_model, pcc_ctx) are owned by
+ *    the library and released with *_destroy.
+ *  - Work is ordered on the ctx's CUDA stream.  Calls return after their output
+ *    lengths are known (each call synchronises the ctx stream at least once).
+ *  - On error no partial output is promised.  On PCC_ERR_CAPACITY the *_len /
+ *    *n_out arguments receive the required size.
+ *  - Coordinates are int32 [n][3] (x, y, z), row-major, each in [0, 2^bit_depth).
+ *    Duplicates are allowed.  Decoded output is the set of unique voxels in Morton
+ *    order (reading Q27), so decode(encode(x)) == sorted_unique(x).
+ */
+#ifndef PCC_H_
+#define PCC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PCC_OK = 0,
+  PCC_ERR_INVALID_ARG = 1,      /* null pointer, bad frame offsets, malformed model file */
+  PCC_ERR_EMPTY = 2,            /* a frame with zero points (SPEC S:669 EmptyCloud) */
+  PCC_ERR_RANGE = 3,            /* a coordinate outside [0, 2^bit_depth) */
+  PCC_ERR_UNSUPPORTED_DEPTH = 4,/* bit_depth outside [max(R+5, min_depth), min(max_depth, 21)] */
+  PCC_ERR_CAPACITY = 5,         /* output buffer too small; required size returned */
+  PCC_ERR_BAD_MAGIC = 6,        /* bitstream does not start with "PCC1" */
+  PCC_ERR_VERSION = 7,          /* unsupported bitstream version */
+  PCC_ERR_MODEL_MISMATCH = 8,   /* bitstream model hash / R / n_deep differ */
+  PCC_ERR_TRUNCATED = 9,        /* bitstream shorter than its header says */
+  PCC_ERR_CORRUPT = 10,         /* inconsistent payload (word counts, states, N_L) */
+  PCC_ERR_CUDA = 11,            /* no sm_100 device or a CUDA runtime failure */
+  PCC_ERR_OOM = 12              /* device allocation failed */
+} pcc_status;
+
+/* Immutable after creation; holds the device-resident int8 weights, int32
+ * biases, requant triples and the exp LUT.  Safe to share between contexts on
+ * the same device. */
+typedef struct pcc_model_s* pcc_model;
+/* Per (device, stream) workspace arena; grows on demand, never shrinks; not
+ * thread-safe.  Reuse one ctx across calls to avoid steady-state allocation. */
+typedef struct pcc_ctx_s* pcc_ctx;
+
+/* Model file = DESIGN.md §4 "Model file" (little-endian, FNV-1a-64 trailer).
+ * Parses, validates the hash, uploads to the current device. */
+pcc_status pcc_model_load(const void* bytes, size_t len, int device, pcc_model* out);
+pcc_status pcc_model_hash(pcc_model m, uint64_t* out);
+/* channels C, head hidden H, raw levels R, deep levels n_deep, min/max depth. */
+pcc_status pcc_model_info(pcc_model m, int* C, int* H, int* R, int* n_deep, int* min_depth, int* max_depth);
+void pcc_model_destroy(pcc_model m);
+
+/* stream: a cudaStream_t cast to void* (NULL = legacy default stream). */
+pcc_status pcc_ctx_create(int device, void* stream, pcc_ctx* out);
+void pcc_ctx_destroy(pcc_ctx c);
+
+/* Worst-case encoded size of one frame of n points (bytes). */
+size_t pcc_encode_bound(size_t n, int bit_depth);
+
+/* Octree of one frame.  d_xyz: device int32 [n][3].  Fills
+ * h_level_counts[bit_depth+1] with the node count N_d of each depth d = 0..L
+ * (N_L = unique voxels) and, if d_codes != NULL, writes the occupancy bytes
+ * X_0 | X_1 | ... | X_{L-1} (depth-major, Morton order) into d_codes
+ * (device, capacity codes_cap bytes; CAPACITY if sum_{d<L} N_d > codes_cap). */
+pcc_status pcc_build_octree(pcc_ctx c, const int32_t* d_xyz, size_t n, int bit_depth,
+                            uint8_t* d_codes, size_t codes_cap, uint32_t* h_level_counts);
+
+/* Encode one frame: d_xyz device int32 [n][3] -> bitstream at d_out (device,
+ * out_cap bytes).  *out_len = bytes written (or required, on CAPACITY). */
+pcc_status pcc_encode(pcc_ctx c, pcc_model m, const int32_t* d_xyz, size_t n, int bit_depth,
+                      uint8_t* d_out, size_t out_cap, size_t* out_len);
+
+/* Decode one bitstream (device bytes d_bs[len]) into d_xyz_out (device int32
+ * [cap_points][3]).  *n_out = unique voxels, *bit_depth_out = L from the header. */
+pcc_status pcc_decode(pcc_ctx c, pcc_model m, const uint8_t* d_bs, size_t len,
+                      int32_t* d_xyz_out, size_t cap_points, size_t* n_out, int* bit_depth_out);
+
+/* Throughput variants: `frames` frames concatenated.  offs / bs_offs are HOST
+ * arrays of frames+1 prefix offsets (points / bytes).  All frames of a batch
+ * share bit_depth.  out_offs (HOST, frames+1) receives the per-frame bitstream
+ * (encode, bytes) or voxel (decode, points) prefix offsets into d_out /
+ * d_xyz_out.  Each frame's bitstream is identical to pcc_encode of that frame
+ * alone; frames start at 4-byte-aligned offsets (zero padding in between). */
+pcc_status pcc_encode_batch(pcc_ctx c, pcc_model m, const int32_t* d_xyz, const size_t* offs, int frames,
+                            int bit_depth, uint8_t* d_out, size_t out_cap, size_t* out_offs);
+pcc_status pcc_decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_offs, int frames,
+                            int32_t* d_xyz_out, size_t cap_points, size_t* out_offs);
+
+/* Host-buffer convenience (end-to-end path): copies h_xyz (host int32 [n][3])
+ * to the device, encodes the batch, copies the bitstreams back into h_out. */
+pcc_status pcc_encode_batch_host(pcc_ctx c, pcc_model m, const int32_t* h_xyz, const size_t* offs, int frames,
+                                 int bit_depth, uint8_t* h_out, size_t out_cap, size_t* out_offs);
+pcc_status pcc_decode_batch_host(pcc_ctx c, pcc_model m, const uint8_t* h_bs, const size_t* bs_offs, int frames,
+                                 int32_t* h_xyz_out, size_t cap_points, size_t* out_offs);
+
+/* Debug / parity: copy a named intermediate tensor of the LAST call on this ctx
+ * (single-frame calls only) to host memory.  Names follow the oracle's dumps:
+ * "key/d" (u64), "code/d" (u8), "nbr/d" (i32 [N][27], absent = -1), "F/d",
+ * "ha/d", "S/d", "G/l/d", "hx/l", "H/l", "Fp/l/d", "a/l" (i8 [N][C or H]),
+ * "cf/l" (u16 pairs cum,freq; encode), "cdf/l" (u16 [N][256] cumulative; decode).
+ * *len = bytes available; copies min(cap, len).  INVALID_ARG if unknown. */
+pcc_status pcc_debug_tensor(pcc_ctx c, const char* name, void* h_dst, size_t cap, size_t* len);
+/* Enable (1) / disable (0) retention of intermediate tensors for
+ * pcc_debug_tensor (adds device->host copies; parity tests only). */
+pcc_status pcc_ctx_set_debug(pcc_ctx c, int on);
+/* Kernel launches issued by the last call on this ctx (own kernels only). */
+uint64_t pcc_ctx_launch_count(pcc_ctx c);
+
+/* Profiling: when on, every kernel launch is bracketed by CUDA events on the ctx
+ * stream and accumulated per category ("sort", "octree", "kmap", "conv", "down",
+ * "up", "head", "rans_enc", "rans_dec", "pack", "expand", ...).  Turning it on or
+ * off resets the totals.  profile_get(category = NULL) returns the sum over
+ * categories.  bytes = algorithmic (compulsory) bytes the launches move
+ * (DESIGN.md §5), for roofline accounting.  Categories: newline-separated list. */
+pcc_status pcc_ctx_set_profile(pcc_ctx c, int on);
+pcc_status pcc_ctx_profile_get(pcc_ctx c, const char* category, double* ms, uint64_t* launches, uint64_t* bytes);
+const char* pcc_ctx_profile_categories(pcc_ctx c);
+
+const char* pcc_status_string(pcc_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCC_H_ */

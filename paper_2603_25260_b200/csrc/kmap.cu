@@ -1,0 +1,104 @@
+// kmap.cu — sparse-conv kernel map via a GPU open-addressing hash table (sparse
+// convolution "decomposed into multiple indexed linear transforms"; the kernel map is the
+// index list of each transform).  Keys carry the frame id above bit 3d, so neighbours
+// never cross frames.  nbr[i][delta] = row of coord(i)+delta, or N (the zero row).
+#include "pcc_internal.cuh"
+
+namespace pcc {
+
+namespace {
+
+constexpr uint64_t EMPTY = ~0ull;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t spread3(uint32_t v) {
+  uint64_t x = v & 0x1fffffu;
+  x = (x | x << 32) & 0x1f00000000ffffull;
+  x = (x | x << 16) & 0x1f0000ff0000ffull;
+  x = (x | x << 8) & 0x100f00f00f00f00full;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+__device__ __forceinline__ uint32_t compact3(uint64_t x) {
+  x &= 0x1249249249249249ull;
+  x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ull;
+  x = (x ^ (x >> 4)) & 0x100f00f00f00f00full;
+  x = (x ^ (x >> 8)) & 0x1f0000ff0000ffull;
+  x = (x ^ (x >> 16)) & 0x1f00000000ffffull;
+  x = (x ^ (x >> 32)) & 0x1fffffull;
+  return uint32_t(x);
+}
+
+__global__ void k_hash_insert(const uint64_t* __restrict__ keys, uint32_t n, unsigned long long* __restrict__ tk,
+                              uint32_t* __restrict__ tv, uint64_t mask) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t k = keys[i];
+  uint64_t h = mix64(k) & mask;
+  while (true) {
+    unsigned long long prev = atomicCAS(&tk[h], (unsigned long long)EMPTY, (unsigned long long)k);
+    if (prev == EMPTY || prev == k) {
+      tv[h] = i;
+      return;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+__global__ void k_kmap(const uint64_t* __restrict__ keys, uint32_t n, int depth, const unsigned long long* __restrict__ tk,
+                       const uint32_t* __restrict__ tv, uint64_t mask, int32_t* __restrict__ nbr) {
+  const size_t t = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= size_t(n) * 27) return;
+  const uint32_t i = uint32_t(t / 27), dl = uint32_t(t % 27);
+  const uint64_t k = keys[i];
+  const int sh = 3 * depth;
+  const uint64_t mbits = sh >= 64 ? ~0ull : ((1ull << sh) - 1ull);
+  const uint64_t fr = sh >= 64 ? 0ull : (k >> sh) << sh;
+  const uint64_t m = k & mbits;
+  const int dx = int(dl / 9) - 1, dy = int((dl / 3) % 3) - 1, dz = int(dl % 3) - 1;
+  const int64_t lim = int64_t(1) << depth;
+  const int64_t X = int64_t(compact3(m >> 2)) + dx, Y = int64_t(compact3(m >> 1)) + dy, Z = int64_t(compact3(m)) + dz;
+  int32_t r = int32_t(n);
+  if (X >= 0 && Y >= 0 && Z >= 0 && X < lim && Y < lim && Z < lim) {
+    const uint64_t q = fr | spread3(uint32_t(X)) << 2 | spread3(uint32_t(Y)) << 1 | spread3(uint32_t(Z));
+    uint64_t h = mix64(q) & mask;
+    while (true) {
+      const unsigned long long s = tk[h];
+      if (s == q) {
+        r = int32_t(tv[h]);
+        break;
+      }
+      if (s == EMPTY) break;
+      h = (h + 1) & mask;
+    }
+  }
+  nbr[t] = r;
+}
+
+}  // namespace
+
+void kernel_map(pcc_ctx c, const uint64_t* keys, uint32_t N, int depth, int32_t* nbr) {
+  if (N == 0) return;
+  uint64_t cap = 1;
+  while (cap < 2ull * N) cap <<= 1;
+  unsigned long long* tk = wsT<unsigned long long>(c, "hash_k", cap);
+  uint32_t* tv = wsT<uint32_t>(c, "hash_v", cap);
+  PCC_CUDA(cudaMemsetAsync(tk, 0xff, cap * sizeof(unsigned long long), c->stream));
+  {
+    Prof p(c, "kmap", size_t(N) * 8 + cap * 12);
+    k_hash_insert<<<(N + 255) / 256, 256, 0, c->stream>>>(keys, N, tk, tv, cap - 1);
+  }
+  size_t t = size_t(N) * 27;
+  {
+    Prof p(c, "kmap", size_t(N) * (8 + 27 * 4));
+    k_kmap<<<unsigned((t + 255) / 256), 256, 0, c->stream>>>(keys, N, depth, tk, tv, cap - 1, nbr);
+  }
+  launched(c, 2);
+}
+
+}  // namespace pcc

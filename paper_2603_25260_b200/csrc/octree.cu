@@ -1,0 +1,420 @@
+// octree.cu — Morton keys, LSD radix sort, per-level occupancy bytes (encoder) and
+// level expansion (decoder).  PAPER.md P:651-660: "sort the input coordinates in Morton
+// order ... repeatedly divide them by 2, apply floor rounding, and remove consecutive
+// duplicates"; occupancy codes = the K2S2 all-ones conv (bit-equivalent OR of child bits);
+// decoder "adding a pre-defined offset matrix ... masking" preserves Morton order.
+//
+// Frames of a batch are sorted together: key = frame << 3L | morton (bits 3L..), so each
+// frame stays contiguous and every depth's node list is frame-major, Morton-minor.
+#include "pcc_internal.cuh"
+
+namespace pcc {
+
+namespace {
+
+__device__ __forceinline__ uint64_t spread3(uint32_t v) {
+  uint64_t x = v & 0x1fffffu;
+  x = (x | x << 32) & 0x1f00000000ffffull;
+  x = (x | x << 16) & 0x1f0000ff0000ffull;
+  x = (x | x << 8) & 0x100f00f00f00f00full;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+__device__ __forceinline__ uint32_t compact3(uint64_t x) {
+  x &= 0x1249249249249249ull;
+  x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ull;
+  x = (x ^ (x >> 4)) & 0x100f00f00f00f00full;
+  x = (x ^ (x >> 8)) & 0x1f0000ff0000ffull;
+  x = (x ^ (x >> 16)) & 0x1f00000000ffffull;
+  x = (x ^ (x >> 32)) & 0x1fffffull;
+  return uint32_t(x);
+}
+
+// ---- a1: Morton keys (x is the MSB of each bit triple, reading O1/Q25) -------------
+__global__ void k_morton(const int32_t* __restrict__ xyz, size_t n, const uint64_t* __restrict__ offs, int B, int L,
+                         uint64_t* __restrict__ keys, uint32_t* __restrict__ err) {
+  size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+  const int32_t lim = 1 << L;
+  if (x < 0 || y < 0 || z < 0 || x >= lim || y >= lim || z >= lim) {
+    atomicOr(err, EF_RANGE);
+    keys[i] = 0;
+    return;
+  }
+  // frame id: largest f with offs[f] <= i
+  int lo = 0, hi = B - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (offs[mid] <= i) lo = mid; else hi = mid - 1;
+  }
+  uint64_t m = spread3(uint32_t(x)) << 2 | spread3(uint32_t(y)) << 1 | spread3(uint32_t(z));
+  keys[i] = (B > 1 ? (uint64_t(lo) << (3 * L)) : 0ull) | m;
+}
+
+// ---- radix sort (LSD, 8-bit digits, stable per pass) ---------------------------------
+constexpr int RS_T = 256, RS_V = 16, RS_TILE = RS_T * RS_V, RS_W = RS_T / 32;
+
+__global__ void __launch_bounds__(RS_T) k_rs_hist(const uint64_t* __restrict__ keys, size_t n, int shift,
+                                                  uint32_t* __restrict__ hist, uint32_t ntiles) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  size_t base = size_t(blockIdx.x) * RS_TILE;
+#pragma unroll 4
+  for (int k = 0; k < RS_V; ++k) {
+    size_t i = base + size_t(k) * RS_T + threadIdx.x;
+    uint32_t d = i < n ? uint32_t((keys[i] >> shift) & 255u) : 256u;
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (d < 256u && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[d], __popc(peers));
+  }
+  __syncthreads();
+  hist[size_t(threadIdx.x) * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(RS_T) k_rs_scatter(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                                     size_t n, int shift, const uint32_t* __restrict__ hscan,
+                                                     uint32_t ntiles) {
+  __shared__ uint32_t wc[RS_W][257];
+  __shared__ uint32_t tstart[256];
+  __shared__ uint32_t gbase[256];
+  __shared__ uint32_t wtot[RS_W];
+  __shared__ uint64_t stage[RS_TILE];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < RS_W * 257; i += RS_T) (&wc[0][0])[i] = 0;
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  uint64_t kv[RS_V];
+  uint32_t rk[RS_V];
+  const size_t wbase = size_t(blockIdx.x) * RS_TILE + size_t(w) * (RS_TILE / RS_W);
+#pragma unroll
+  for (int t = 0; t < RS_V; ++t) {
+    size_t i = wbase + size_t(t) * 32 + lane;
+    uint64_t k = i < n ? in[i] : 0ull;
+    uint32_t d = i < n ? uint32_t((k >> shift) & 255u) : 256u;
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    uint32_t base = wc[w][d];
+    __syncwarp();
+    if (lane == __ffs(peers) - 1) wc[w][d] = base + __popc(peers);
+    __syncwarp();
+    kv[t] = k;
+    rk[t] = (d << 16) | (base + __popc(peers & lt));  // rank < 4096 fits 16 bits
+  }
+  __syncthreads();
+  // per-digit exclusive prefix over warps; tile count per digit
+  uint32_t run = 0;
+  for (int ww = 0; ww < RS_W; ++ww) {
+    uint32_t t = wc[ww][threadIdx.x];
+    wc[ww][threadIdx.x] = run;
+    run += t;
+  }
+  // exclusive scan of run over the 256 digits (one per thread)
+  uint32_t inc = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) wtot[w] = inc;
+  __syncthreads();
+  uint32_t wpre = 0;
+  for (int ww = 0; ww < w; ++ww) wpre += wtot[ww];
+  tstart[threadIdx.x] = wpre + inc - run;
+  gbase[threadIdx.x] = hscan[size_t(threadIdx.x) * ntiles + blockIdx.x];
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < RS_V; ++t) {
+    uint32_t d = rk[t] >> 16;
+    if (d < 256u) stage[tstart[d] + wc[w][d] + (rk[t] & 0xffffu)] = kv[t];
+  }
+  __syncthreads();
+  const size_t tb = size_t(blockIdx.x) * RS_TILE;
+  const uint32_t nvalid = uint32_t((n - tb) < size_t(RS_TILE) ? (n - tb) : size_t(RS_TILE));
+  for (uint32_t p = threadIdx.x; p < nvalid; p += RS_T) {
+    uint64_t k = stage[p];
+    uint32_t d = uint32_t((k >> shift) & 255u);
+    out[gbase[d] + p - tstart[d]] = k;
+  }
+}
+
+// ---- a2: all levels at once from the sorted leaf keys --------------------------------
+// lvl(i) = first depth at which sorted key i starts a new node (its key differs from key
+// i-1 above bit 3(L-d)); duplicates get L+1.  N_d = #{i : lvl(i) <= d}.
+__device__ __forceinline__ int leaf_lvl(const uint64_t* keys, size_t i, int L) {
+  if (i == 0) return 0;
+  uint64_t x = keys[i] ^ keys[i - 1];
+  if (x == 0) return L + 1;
+  int hb = 63 - __clzll((long long)x);
+  int l = L - hb / 3;
+  return l < 0 ? 0 : l;
+}
+
+constexpr int LV_T = 256, LV_R = 4, LV_TILE = LV_T * LV_R, LV_W = LV_T / 32;
+
+__global__ void __launch_bounds__(LV_T) k_lvl_count(const uint64_t* __restrict__ keys, size_t n, int L,
+                                                    uint32_t* __restrict__ cnt, uint32_t nblk) {
+  __shared__ uint32_t h[MAX_DEPTH + 2];
+  if (threadIdx.x < MAX_DEPTH + 2) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int r = 0; r < LV_R; ++r) {
+    size_t i = size_t(blockIdx.x) * LV_TILE + size_t(r) * LV_T + threadIdx.x;
+    if (i < n) atomicAdd(&h[leaf_lvl(keys, i, L)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x <= L) {
+    uint32_t s = 0;
+    for (int l = 0; l <= int(threadIdx.x); ++l) s += h[l];
+    cnt[size_t(threadIdx.x) * nblk + blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(LV_T) k_lvl_scatter(const uint64_t* __restrict__ keys, size_t n, int L, int B,
+                                                      const uint32_t* __restrict__ off, uint32_t nblk,
+                                                      uint64_t* __restrict__ key_all, uint8_t* __restrict__ code_all,
+                                                      uint32_t* __restrict__ cs_all, uint32_t* __restrict__ par_all,
+                                                      uint32_t* __restrict__ foff) {
+  __shared__ uint32_t wcnt[LV_W][MAX_DEPTH + 1];
+  __shared__ uint32_t run[MAX_DEPTH + 1];
+  __shared__ uint32_t nbs[MAX_DEPTH + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x <= L) {
+    run[threadIdx.x] = off[size_t(threadIdx.x) * nblk + blockIdx.x];  // global index base (incl. nb[d])
+    nbs[threadIdx.x] = off[size_t(threadIdx.x) * nblk];                // nb[d]
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  for (int r = 0; r < LV_R; ++r) {
+    size_t i = size_t(blockIdx.x) * LV_TILE + size_t(r) * LV_T + threadIdx.x;
+    const bool valid = i < n;
+    const int lvl = valid ? leaf_lvl(keys, i, L) : L + 1;
+    const uint64_t key = valid ? keys[i] : 0ull;
+    uint32_t rk[MAX_DEPTH + 1];
+#pragma unroll
+    for (int d = 0; d <= MAX_DEPTH; ++d) {
+      if (d > L) break;
+      unsigned b = __ballot_sync(0xffffffffu, lvl <= d);
+      rk[d] = __popc(b & lt);
+      if (lane == 0) wcnt[w][d] = __popc(b);
+    }
+    __syncthreads();
+    // excl_d(i) = run[d] + sum of earlier warps + rank  (global index incl. nb[d])
+    uint32_t ex[MAX_DEPTH + 1];
+#pragma unroll
+    for (int d = 0; d <= MAX_DEPTH; ++d) {
+      if (d > L) break;
+      uint32_t s = run[d];
+      for (int ww = 0; ww < w; ++ww) s += wcnt[ww][d];
+      ex[d] = s + rk[d] - nbs[d];  // local index within depth d
+    }
+    if (valid && lvl <= L) {
+      const int f = (B > 1) ? int(key >> (3 * L)) : 0;
+#pragma unroll
+      for (int d = 0; d <= MAX_DEPTH; ++d) {
+        if (d > L) break;
+        if (d < lvl) continue;
+        const size_t g = size_t(nbs[d]) + ex[d];
+        key_all[g] = key >> (3 * (L - d));
+        if (d < L) cs_all[g] = ex[d + 1];
+        if (d >= 1) {
+          const uint32_t p = ex[d - 1] - (lvl == d ? 1u : 0u);
+          par_all[g] = p;
+          const size_t gp = size_t(nbs[d - 1]) + p;
+          const uint32_t bit = 1u << uint32_t((key >> (3 * (L - d))) & 7u);
+          atomicOr(reinterpret_cast<unsigned*>(code_all + (gp & ~size_t(3))), bit << (8 * (gp & 3)));
+        }
+        if (lvl == 0) foff[size_t(d) * (B + 1) + f] = ex[d];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x <= L) {
+      uint32_t s = 0;
+      for (int ww = 0; ww < LV_W; ++ww) s += wcnt[ww][threadIdx.x];
+      run[threadIdx.x] += s;
+    }
+    __syncthreads();
+  }
+}
+
+// counts[d] = N_d, foff[d][B] = N_d
+__global__ void k_lvl_totals(const uint32_t* __restrict__ off, uint32_t nblk, int L, int B, uint32_t* __restrict__ counts,
+                             uint32_t* __restrict__ foff) {
+  int d = threadIdx.x;
+  if (d > L) return;
+  uint32_t lo = off[size_t(d) * nblk], hi = off[size_t(d + 1) * nblk];
+  counts[d] = hi - lo;
+  foff[size_t(d) * (B + 1) + B] = hi - lo;
+}
+
+// ---- a2': decoder expansion -------------------------------------------------------
+__global__ void k_popc(const uint8_t* __restrict__ X, uint32_t n, uint32_t* __restrict__ out) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __popc(uint32_t(X[i]));
+}
+
+__global__ void k_expand(const uint64_t* __restrict__ key_d, const uint8_t* __restrict__ X, const uint32_t* __restrict__ cs,
+                         uint32_t n, uint64_t* __restrict__ key_c, uint32_t* __restrict__ par_c) {
+  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  uint32_t x = X[p], j = cs[p];
+  const uint64_t k = key_d[p] << 3;
+  for (int c = 0; c < 8; ++c)
+    if ((x >> c) & 1u) {
+      key_c[j] = k | uint64_t(c);
+      par_c[j] = p;
+      ++j;
+    }
+}
+
+__global__ void k_foff_next(const uint32_t* __restrict__ cs, const uint32_t* __restrict__ foff_d, int B,
+                            uint32_t* __restrict__ foff_n) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f <= B) foff_n[f] = cs[foff_d[f]];
+}
+
+__global__ void k_keys_to_xyz(const uint64_t* __restrict__ keys, size_t n, int L, int32_t* __restrict__ xyz) {
+  size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t m = keys[i] & ((L >= 21) ? ~0ull >> 1 : ((1ull << (3 * L)) - 1ull));
+  xyz[3 * i] = int32_t(compact3(m >> 2));
+  xyz[3 * i + 1] = int32_t(compact3(m >> 1));
+  xyz[3 * i + 2] = int32_t(compact3(m));
+}
+
+inline unsigned cdiv(size_t a, size_t b) { return unsigned((a + b - 1) / b); }
+
+}  // namespace
+
+void build_octree(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int B, int L, OctreeOut& o) {
+  const size_t n = offs[B];
+  cudaStream_t s = c->stream;
+  // device copy of frame offsets
+  uint64_t* d_offs = wsT<uint64_t>(c, "oct_offs", B + 1);
+  uint64_t* h = static_cast<uint64_t*>(pinned(c, (B + 1) * sizeof(uint64_t)));
+  for (int f = 0; f <= B; ++f) h[f] = offs[f];
+  PCC_CUDA(cudaMemcpyAsync(d_offs, h, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  uint32_t* err = wsT<uint32_t>(c, "err", 4);
+  PCC_CUDA(cudaMemsetAsync(err, 0, 4 * sizeof(uint32_t), s));
+
+  uint64_t* ka = wsT<uint64_t>(c, "sort_a", n);
+  uint64_t* kb = wsT<uint64_t>(c, "sort_b", n);
+  {
+    Prof p(c, "morton", n * 20);
+    k_morton<<<cdiv(n, 256), 256, 0, s>>>(d_xyz, n, d_offs, B, L, ka, err);
+    launched(c);
+  }
+
+  int fb = 0;
+  while ((1 << fb) < B) ++fb;
+  const int bits = 3 * L + fb;
+  const uint32_t ntiles = cdiv(n, RS_TILE);
+  uint32_t* hist = wsT<uint32_t>(c, "rs_hist", size_t(256) * ntiles + 1);
+  for (int sh = 0; sh < bits; sh += 8) {
+    {
+      Prof p(c, "sort", n * 8);
+      k_rs_hist<<<ntiles, RS_T, 0, s>>>(ka, n, sh, hist, ntiles);
+      launched(c);
+    }
+    scan_u32(c, hist, hist, size_t(256) * ntiles);
+    {
+      Prof p(c, "sort", n * 16);
+      k_rs_scatter<<<ntiles, RS_T, 0, s>>>(ka, kb, n, sh, hist, ntiles);
+      launched(c);
+    }
+    std::swap(ka, kb);
+  }
+  const uint64_t* sorted = ka;
+
+  const uint32_t nblk = cdiv(n, LV_TILE);
+  uint32_t* cnt = wsT<uint32_t>(c, "lv_cnt", size_t(L + 1) * nblk + 1);
+  {
+    Prof p(c, "octree", n * 8);
+    k_lvl_count<<<nblk, LV_T, 0, s>>>(sorted, n, L, cnt, nblk);
+    launched(c);
+  }
+  scan_u32(c, cnt, cnt, size_t(L + 1) * nblk);
+  // sizes: total nodes over all depths <= (L+1) n
+  uint32_t* small = wsT<uint32_t>(c, "lv_small", (L + 1) + size_t(L + 1) * (B + 1));
+  uint32_t* d_counts = small;
+  uint32_t* d_foff = wsT<uint32_t>(c, "foff", size_t(L + 2) * (B + 1));
+  {
+    Prof p(c, "octree", 0);
+    k_lvl_totals<<<1, 32, 0, s>>>(cnt, nblk, L, B, d_counts, d_foff);
+  }
+  launched(c);
+  // read totals to size the node arrays (sync #1)
+  uint32_t* hc = static_cast<uint32_t*>(pinned(c, (L + 2) * sizeof(uint32_t)));
+  PCC_CUDA(cudaMemcpyAsync(hc, d_counts, (L + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  PCC_CUDA(cudaMemcpyAsync(hc + L + 1, err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  PCC_CUDA(cudaStreamSynchronize(s));
+  if (hc[L + 1] & EF_RANGE) throw Error{PCC_ERR_RANGE};
+  o.N.assign(hc, hc + L + 1);
+  o.nb.assign(L + 2, 0);
+  for (int d = 0; d <= L; ++d) o.nb[d + 1] = o.nb[d] + o.N[d];
+  const size_t tot = o.nb[L + 1];
+  uint64_t* key_all = wsT<uint64_t>(c, "key", tot);
+  uint8_t* code_all = wsT<uint8_t>(c, "code", tot + 8);
+  uint32_t* cs_all = wsT<uint32_t>(c, "cs", tot);
+  uint32_t* par_all = wsT<uint32_t>(c, "par", tot);
+  PCC_CUDA(cudaMemsetAsync(code_all, 0, tot + 8, s));
+  {
+    Prof p(c, "octree", n * 8 + tot * (8 + 1 + 4 + 4));
+    k_lvl_scatter<<<nblk, LV_T, 0, s>>>(sorted, n, L, B, cnt, nblk, key_all, code_all, cs_all, par_all, d_foff);
+    launched(c);
+  }
+  // host copy of frame offsets (for rANS segment layout)
+  uint32_t* hf = static_cast<uint32_t*>(pinned(c, size_t(L + 1) * (B + 1) * sizeof(uint32_t)));
+  PCC_CUDA(cudaMemcpyAsync(hf, d_foff, size_t(L + 1) * (B + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  PCC_CUDA(cudaStreamSynchronize(s));
+  o.foff.assign(hf, hf + size_t(L + 1) * (B + 1));
+}
+
+uint32_t expand_level(pcc_ctx c, int d, int B, OctreeOut& o, uint32_t max_nodes) {
+  cudaStream_t s = c->stream;
+  const uint32_t n = o.N[d];
+  uint64_t* key_all = static_cast<uint64_t*>(c->bufs.at("key").p);
+  uint8_t* code_all = static_cast<uint8_t*>(c->bufs.at("code").p);
+  uint32_t* cs_all = static_cast<uint32_t*>(c->bufs.at("cs").p);
+  uint32_t* par_all = static_cast<uint32_t*>(c->bufs.at("par").p);
+  uint32_t* d_foff = static_cast<uint32_t*>(c->bufs.at("foff").p);
+  uint32_t* cs = cs_all + o.nb[d];
+  uint32_t* tmp = wsT<uint32_t>(c, "exp_tmp", size_t(n) + 1);
+  {
+    Prof p(c, "expand", size_t(n) * 5);
+    k_popc<<<cdiv(n, 256), 256, 0, s>>>(code_all + o.nb[d], n, tmp);
+    launched(c);
+  }
+  scan_u32(c, tmp, tmp, n);
+  PCC_CUDA(cudaMemcpyAsync(cs, tmp, (size_t(n) + 1) * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+  uint32_t* hn = static_cast<uint32_t*>(pinned(c, 4));
+  PCC_CUDA(cudaMemcpyAsync(hn, tmp + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  PCC_CUDA(cudaStreamSynchronize(s));
+  const uint32_t nn = *hn;
+  if (nn > max_nodes) throw Error{PCC_ERR_CORRUPT};
+  o.N.resize(d + 2);
+  o.N[d + 1] = nn;
+  o.nb.resize(d + 3);
+  o.nb[d + 2] = o.nb[d + 1] + nn;
+  if (o.nb[d + 2] > c->bufs.at("key").cap / sizeof(uint64_t)) throw Error{PCC_ERR_CORRUPT};
+  Prof pe(c, "expand", size_t(n) * 13 + size_t(nn) * 12);
+  k_expand<<<cdiv(n, 256), 256, 0, s>>>(key_all + o.nb[d], code_all + o.nb[d], cs, n, key_all + o.nb[d + 1],
+                                        par_all + o.nb[d + 1]);
+  launched(c);
+  Prof pf(c, "expand", 0);
+  k_foff_next<<<cdiv(B + 1, 256), 256, 0, s>>>(cs, d_foff + size_t(d) * (B + 1), B, d_foff + size_t(d + 1) * (B + 1));
+  launched(c);
+  uint32_t* hf = static_cast<uint32_t*>(pinned(c, (B + 1) * sizeof(uint32_t)));
+  PCC_CUDA(cudaMemcpyAsync(hf, d_foff + size_t(d + 1) * (B + 1), (B + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  PCC_CUDA(cudaStreamSynchronize(s));
+  o.foff.resize(size_t(d + 2) * (B + 1));
+  for (int f = 0; f <= B; ++f) o.foff[size_t(d + 1) * (B + 1) + f] = hf[f];
+  return nn;
+}
+
+void keys_to_xyz(pcc_ctx c, const uint64_t* keys, size_t n, int L, int32_t* xyz) {
+  if (!n) return;
+  Prof p(c, "expand", n * 20);
+  k_keys_to_xyz<<<cdiv(n, 256), 256, 0, c->stream>>>(keys, n, L, xyz);
+  launched(c);
+}
+
+}  // namespace pcc

@@ -1,0 +1,213 @@
+// pcc_internal.cuh — shared declarations of the CUDA path (sm_100a).
+// Nothing here is shared with oracle/: the two implementations are independent.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/pcc.h"
+
+namespace pcc {
+
+constexpr int NCODE = 255;     // occupancy classes
+constexpr int SEG_SYMS = 65536; // rANS segment length (reading Q24)
+constexpr int MAX_LANES = 32;
+constexpr int MAX_DEPTH = 21;   // 63-bit Morton key cap
+
+// Device error flags (atomicOr'ed by kernels, read at sync points).
+enum : uint32_t {
+  EF_RANGE = 1u << 0,
+  EF_CORRUPT = 1u << 1,
+};
+
+struct RQ {  // fixed-point requant, Eq.14; m_neg != m_pos = fused PReLU (reading Q18)
+  int32_t mp, mn, r;
+};
+
+struct DConv {       // K3S1 conv: W [27][cout][cin], b [cout]
+  const int8_t* W;
+  const int32_t* b;
+  RQ rq;
+};
+struct DUp {         // Upsampling over Concat(S, onehot X): W_S [8C][C], E [255][8C] (= q_one*W_X), b [8C]
+  const int8_t* W;
+  const int32_t* E;
+  const int32_t* b;
+  RQ rq;
+};
+struct DHead {       // Predictor: W1 [H][C], b1, rq1; W2 [256][H] (row 255 = 0), b2 [256]; logit rq
+  const int8_t* W1;
+  const int32_t* b1;
+  RQ rq1;
+  const int8_t* W2;
+  const int32_t* b2;
+  RQ rql;
+};
+struct DShallow {
+  DConv a, b;
+  int32_t k_s;
+  DUp up;
+  DHead head;
+};
+struct DDown {       // K2S2: W [8][C][C], b [C]
+  const int8_t* W;
+  const int32_t* b;
+  RQ rq;
+};
+struct DDeep {
+  const int8_t* E;   // [255][C]
+  DDown down[3];
+  DConv a;           // [27][C][2C]
+  DConv b;           // [27][C][C]
+  const int8_t* P;   // [C][2C]
+  DUp up[4];
+  DHead head;
+};
+
+}  // namespace pcc
+
+struct pcc_model_s {
+  int device = 0;
+  int C = 0, H = 0, R = 0, n_deep = 0, min_depth = 0, max_depth = 0;
+  uint64_t hash = 0;
+  void* dmem = nullptr;
+  const uint32_t* lut = nullptr;
+  const int8_t* E0 = nullptr;
+  std::vector<pcc::DShallow> shallow;  // index d - R
+  std::vector<pcc::DDeep> deep;        // index j - 1
+};
+
+struct pcc_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  std::map<std::string, Buf> bufs;
+  void* pinned = nullptr;
+  size_t pinned_cap = 0;
+  bool debug = false;
+  std::map<std::string, std::vector<uint8_t>> dbg;
+  uint64_t launches = 0;
+  // per-category CUDA-event timing of launches (pcc_ctx_set_profile)
+  bool prof = false;
+  struct Rec {
+    std::string cat;
+    cudaEvent_t a, b;
+    uint64_t bytes;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  struct Tot {
+    double ms = 0;
+    uint64_t launches = 0, bytes = 0;
+  };
+  std::map<std::string, Tot> tot;
+};
+
+namespace pcc {
+
+struct Error {
+  pcc_status st;
+};
+
+#define PCC_CUDA(x)                                      \
+  do {                                                   \
+    cudaError_t e_ = (x);                                \
+    if (e_ != cudaSuccess) throw ::pcc::Error{e_ == cudaErrorMemoryAllocation ? PCC_ERR_OOM : PCC_ERR_CUDA}; \
+  } while (0)
+
+// Workspace arena: named buffers, grown on demand, never shrunk.
+void* ws(pcc_ctx c, const char* name, size_t bytes);
+template <class T>
+T* wsT(pcc_ctx c, const char* name, size_t count) {
+  return static_cast<T*>(ws(c, name, count * sizeof(T) + 16));
+}
+void* pinned(pcc_ctx c, size_t bytes);
+void launched(pcc_ctx c, int n = 1);
+
+// Scoped event pair around one launch of category `cat` (only when profiling is on).
+// `bytes` = algorithmic (compulsory) bytes the launch moves, for roofline accounting.
+struct Prof {
+  pcc_ctx c;
+  const char* cat;
+  uint64_t bytes;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Prof(pcc_ctx c_, const char* cat_, uint64_t bytes_);
+  ~Prof();
+};
+void prof_collect(pcc_ctx c);
+void dbg_copy(pcc_ctx c, const std::string& name, const void* dptr, size_t bytes);
+
+// ---- scan.cu ----
+// Exclusive scan of n u32 values; out[n] receives the total.  in may equal out.
+void scan_u32(pcc_ctx c, const uint32_t* in, uint32_t* out, size_t n);
+
+// ---- octree.cu ----
+struct OctreeOut {            // concatenated across depths; node arrays indexed nb[d] + local
+  std::vector<uint32_t> N;    // N[d], d = 0..L (totals over frames)
+  std::vector<uint64_t> nb;   // base offset of depth d in the concatenated arrays
+  std::vector<uint32_t> foff; // host copy: foff[d*(B+1) + f] local index of frame f's first node at depth d
+};
+// Encoder: Morton keys + radix sort + all levels.  Fills ctx buffers
+// "key" (u64), "code" (u8), "cs" (u32 child start, local), "par" (u32 parent, local),
+// "foff" (u32 [(L+1)*(B+1)]).
+void build_octree(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int B, int L, OctreeOut& o);
+// Decoder: expand depth d -> d+1 from decoded codes (arrays as above).  Returns N_{d+1}.
+uint32_t expand_level(pcc_ctx c, int d, int B, OctreeOut& o, uint32_t max_nodes);
+// Morton-decode depth-L keys of all frames into xyz (frame bits dropped).
+void keys_to_xyz(pcc_ctx c, const uint64_t* keys, size_t n, int L, int32_t* xyz);
+
+// ---- kmap.cu ----
+// nbr[N][27] for the N nodes of one depth (keys include frame bits); absent -> N.
+void kernel_map(pcc_ctx c, const uint64_t* keys, uint32_t N, int depth, int32_t* nbr);
+
+// ---- nn.cu ----
+void embed(pcc_ctx c, const int8_t* E, const uint8_t* X, uint32_t n, int C, int8_t* out);
+// out = act(conv3([in0 | in1]) + skip + b) with the zero row written at index n.
+//   skip_mode 0: none; 1: k_s * skip0[i]; 2: P [cout][2C] * [skip0 | skip1][i]
+void conv3(pcc_ctx c, const int8_t* in0, const int8_t* in1, int C, uint32_t n, const int32_t* nbr,
+           const DConv& L, int skip_mode, const int8_t* skip0, const int8_t* skip1, int32_t k_s, const int8_t* P,
+           int8_t* out);
+void down(pcc_ctx c, const int8_t* g, const uint8_t* Xp, const uint32_t* cs_p, uint32_t np, int C, const DDown& L,
+          int8_t* out);
+void up_prune(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* par_c, const uint64_t* key_c,
+              uint32_t nc, int C, const DUp& L, int8_t* out);
+// mode 0: encoder -> cf[n] (cum | freq<<16) for true symbols X; mode 1: decoder -> cdf rows u16[n][256]
+void head_cdf(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
+              const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg);
+
+// ---- rans.cu ----
+struct EncSeg {      // one rANS segment of the encoder
+  uint32_t node;     // first symbol (index into the concatenated cf / code arrays)
+  uint32_t n;        // symbols
+};
+void rans_encode(pcc_ctx c, const EncSeg* d_segs, int nseg, const uint32_t* cf, uint16_t* words, uint32_t* seg_W,
+                 uint32_t* seg_state);
+struct DecSeg {
+  uint64_t byte;     // offset of the segment's level payload in the bitstream buffer
+  uint32_t chunk;    // segment index within the level payload
+  uint32_t node;     // first symbol (local index within the depth)
+  uint32_t n;        // symbols
+  uint32_t level_bytes;
+  uint32_t last;     // 1 if this is the level's last segment (must end the payload)
+};
+void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf, uint8_t* X,
+                 uint32_t* err);
+
+// ---- pack (runtime.cu) ----
+struct PackItem {    // encoder output item: frame header+raw prefix (kind 0) or one segment (kind 1)
+  uint32_t kind;
+  uint32_t frame;
+  uint32_t seg;      // kind 1: encoder segment index
+  uint32_t level;    // kind 1: coded depth d
+  uint32_t bytes;    // kind 0: header + padded raw prefix bytes
+  uint32_t nitems;   // kind 0: items of this frame (header + its segments)
+};
+
+}  // namespace pcc

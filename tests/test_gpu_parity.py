@@ -1,0 +1,287 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, tolerance 0.
+
+The pipeline is integer-only, so every intermediate tensor, every CDF and every
+bitstream must be bit-identical (BASELINE.json north_star).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402
+from paper_2603_25260_b200 import inputs as I  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def pcc():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2603_25260_b200 import pcc as P
+    return P
+
+
+_models = {}
+
+
+def model_pair(C, max_depth=18, kind="random", seed=1):
+    key = (C, max_depth, kind, seed)
+    if key not in _models:
+        mb = I.make_model(C=C, H=C, seed=seed, min_depth=9, max_depth=max_depth, kind=kind).to_bytes()
+        _models[key] = (mb, O.Model(mb))
+    return _models[key]
+
+
+@pytest.fixture(scope="module")
+def ctx(pcc):
+    c = pcc.pcc_ctx_create(0, torch.cuda.current_stream().cuda_stream)
+    yield c
+    pcc.pcc_ctx_destroy(c)
+
+
+_gpu_models = {}
+
+
+def gpu_model(pcc, mb):
+    h = hash(mb)
+    if h not in _gpu_models:
+        _gpu_models[h] = pcc.pcc_model_load(mb, 0)
+    return _gpu_models[h]
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_encode(pcc, ctx, m, frames, L):
+    offs = np.cumsum([0] + [len(f) for f in frames]).tolist()
+    x = dev(np.concatenate(frames).astype(np.int32))
+    cap = sum(pcc.pcc_encode_bound(len(f), L) + 4 for f in frames)
+    out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    oo = pcc.pcc_encode_batch(ctx, m, x, offs, L, out, cap)
+    host = out[:oo[-1]].cpu().numpy().tobytes()
+    return [host[oo[i]:oo[i + 1]] for i in range(len(frames))], oo
+
+
+def gpu_decode(pcc, ctx, m, streams, cap_points):
+    offs = [0]
+    blob = b""
+    for s in streams:
+        blob += s + bytes((-len(s)) % 4)
+        offs.append(len(blob))
+    d = dev(np.frombuffer(blob, np.uint8))
+    out = torch.empty((cap_points, 3), dtype=torch.int32, device="cuda")
+    oo = pcc.pcc_decode_batch(ctx, m, d, offs, out, cap_points)
+    xyz = out[:oo[-1]].cpu().numpy()
+    return [xyz[oo[i]:oo[i + 1]] for i in range(len(streams))]
+
+
+def morton_sorted_unique(pts, L):
+    keys, _ = O.build_octree(pts, L)
+    k = keys[L].astype(np.uint64)
+    out = np.zeros((k.size, 3), np.int64)
+    for b in range(L):
+        t = (k >> np.uint64(3 * b)) & np.uint64(7)
+        out[:, 0] |= ((t >> np.uint64(2)) & np.uint64(1)).astype(np.int64) << b
+        out[:, 1] |= ((t >> np.uint64(1)) & np.uint64(1)).astype(np.int64) << b
+        out[:, 2] |= (t & np.uint64(1)).astype(np.int64) << b
+    return out.astype(np.int32)
+
+
+# ---------------------------------------------------------------------------------------
+# octree (a1, a2)
+# ---------------------------------------------------------------------------------------
+
+def _octree_cases():
+    g = np.arange(2, dtype=np.int32)
+    cube = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+    rng = np.random.default_rng(0)
+    dup = I.random_cloud(1000, 10, 3)
+    dup = np.concatenate([dup, dup[rng.integers(0, 1000, 2000)]])[rng.permutation(3000)]
+    return [("single", np.array([[5, 6, 7]], np.int32), 9), ("cube", cube, 1), ("dups", dup, 10),
+            ("cfg1", I.make_frame(I.CFG1), 12), ("cfg2", I.make_frame(I.CFG2), 12),
+            ("cfg3", I.make_frame(I.CFG3), 18), ("L21", I.random_cloud(5000, 21, 4), 21),
+            ("ragged", I.random_cloud(4097, 12, 5), 12)]
+
+
+@pytest.mark.parametrize("name,pts,L", _octree_cases(), ids=lambda v: v if isinstance(v, str) else "")
+def test_build_octree(pcc, ctx, name, pts, L):
+    keys, codes = O.build_octree(pts, L)
+    tot = sum(len(c) for c in codes)
+    d_codes = torch.empty(tot + 16, dtype=torch.uint8, device="cuda")
+    counts = pcc.pcc_build_octree(ctx, dev(pts.astype(np.int32)), len(pts), L, d_codes, tot + 16)
+    assert counts == [len(k) for k in keys]
+    assert np.array_equal(d_codes[:tot].cpu().numpy(), np.concatenate(codes))
+
+
+def test_build_octree_errors(pcc, ctx):
+    with pytest.raises(pcc.PCCError) as e:
+        pcc.pcc_build_octree(ctx, dev(np.array([[0, 0, 4096]], np.int32)), 1, 12)
+    assert e.value.name == "RANGE"
+
+
+# ---------------------------------------------------------------------------------------
+# per-tensor parity of the encoder (a3-a9)
+# ---------------------------------------------------------------------------------------
+
+def _compare_dumps(pcc, ctx, D, L, R=4):
+    names = D.names()
+    checked = 0
+    for name in names:
+        kind = name.split("/")[0]
+        if kind in ("p", "seg", "z"):
+            continue
+        want = D.get(name, np.uint8)
+        got = pcc.pcc_debug_tensor(ctx, name)
+        assert got is not None, name
+        got = np.frombuffer(got, np.uint8)
+        if kind == "nbr":
+            g = got.view(np.int32).copy()
+            n = g.size // 27
+            g[g == n] = -1
+            got = g.view(np.uint8)
+        assert got.size == want.size, (name, got.size, want.size)
+        if not np.array_equal(got, want):
+            bad = np.flatnonzero(got != want)
+            raise AssertionError(f"{name}: {bad.size} bytes differ, first at {bad[:8]}")
+        checked += 1
+    return checked
+
+
+@pytest.mark.parametrize("C,cfg", [(8, "cfg1"), (32, "cfg1"), (32, "random10")])
+def test_encoder_per_tensor_parity(pcc, ctx, C, cfg):
+    mb, om = model_pair(C)
+    m = gpu_model(pcc, mb)
+    if cfg == "cfg1":
+        pts, L = I.make_frame(I.CFG1), 12
+    else:
+        pts, L = I.random_cloud(4000, 10, 11, spread=0.3), 10
+    D = O.Dump()
+    want = O.encode(om, pts, L, D)
+    pcc.pcc_ctx_set_debug(ctx, True)
+    try:
+        got, _ = gpu_encode(pcc, ctx, m, [pts], L)
+        n = _compare_dumps(pcc, ctx, D, L)
+    finally:
+        pcc.pcc_ctx_set_debug(ctx, False)
+    assert n > 40
+    assert got[0] == want
+
+
+def test_decoder_cdf_parity(pcc, ctx):
+    mb, om = model_pair(8)
+    m = gpu_model(pcc, mb)
+    pts = I.make_frame(I.CFG1)
+    D = O.Dump()
+    bs = O.encode(om, pts, 12, D)
+    pcc.pcc_ctx_set_debug(ctx, True)
+    try:
+        out = gpu_decode(pcc, ctx, m, [bs], len(pts))
+        for d in range(4, 12):
+            p = D.get(f"p/{d}", np.uint16).reshape(-1, 255).astype(np.int64)
+            cum = np.concatenate([np.zeros((p.shape[0], 1), np.int64), np.cumsum(p, 1)[:, :254],
+                                  np.full((p.shape[0], 1), 0xFFFF)], 1).astype(np.uint16)
+            got = np.frombuffer(pcc.pcc_debug_tensor(ctx, f"cdf/{d}"), np.uint16).reshape(-1, 256)
+            assert np.array_equal(got, cum), d
+            assert np.array_equal(np.frombuffer(pcc.pcc_debug_tensor(ctx, f"code/{d}"), np.uint8),
+                                  D.get(f"code/{d}", np.uint8)), d
+    finally:
+        pcc.pcc_ctx_set_debug(ctx, False)
+    assert np.array_equal(out[0], morton_sorted_unique(pts, 12))
+
+
+# ---------------------------------------------------------------------------------------
+# end-to-end bitstreams (a10-a12) at the benchmark's sizes and launch configuration
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg,C,B", [("cfg1", 8, 7), ("cfg2", 32, 4), ("cfg3", 32, 1)])
+def test_batch_bitstreams_match_oracle(pcc, ctx, cfg, C, B):
+    sc = I.CONFIGS[cfg]
+    mb, om = model_pair(C)
+    m = gpu_model(pcc, mb)
+    frames = I.make_frames(sc, B, first=3)
+    got, _ = gpu_encode(pcc, ctx, m, frames, sc.bit_depth)
+    for f, g in zip(frames, got):
+        assert g == O.encode(om, f, sc.bit_depth)
+    dec = gpu_decode(pcc, ctx, m, got, sum(len(f) for f in frames))
+    for f, x in zip(frames, dec):
+        assert np.array_equal(x, morton_sorted_unique(f, sc.bit_depth))
+
+
+def test_batch_equals_single_and_deterministic(pcc, ctx):
+    mb, om = model_pair(8)
+    m = gpu_model(pcc, mb)
+    frames = [I.random_cloud(n, 11, s) for s, n in [(1, 1), (2, 700), (3, 5000), (4, 64)]]
+    batch, _ = gpu_encode(pcc, ctx, m, frames, 11)
+    again, _ = gpu_encode(pcc, ctx, m, frames, 11)
+    assert batch == again
+    for f, b in zip(frames, batch):
+        single, _ = gpu_encode(pcc, ctx, m, [f], 11)
+        assert single[0] == b == O.encode(om, f, 11)
+
+
+def test_zero_model_and_max_depth(pcc, ctx):
+    mb, om = model_pair(8, max_depth=21, kind="zero")
+    m = gpu_model(pcc, mb)
+    pts = I.random_cloud(3000, 21, 9, spread=0.001)
+    got, _ = gpu_encode(pcc, ctx, m, [pts], 21)
+    assert got[0] == O.encode(om, pts, 21)
+    dec = gpu_decode(pcc, ctx, m, got, len(pts))
+    assert np.array_equal(dec[0], morton_sorted_unique(pts, 21))
+
+
+def test_large_level_multi_segment(pcc, ctx):
+    """A level with > 65536 nodes spans several rANS segments (reading Q24)."""
+    mb, om = model_pair(8, max_depth=12)
+    m = gpu_model(pcc, mb)
+    pts = I.random_cloud(150000, 12, 21)
+    got, _ = gpu_encode(pcc, ctx, m, [pts], 12)
+    assert got[0] == O.encode(om, pts, 12)
+    dec = gpu_decode(pcc, ctx, m, got, len(pts))
+    assert np.array_equal(dec[0], morton_sorted_unique(pts, 12))
+
+
+# ---------------------------------------------------------------------------------------
+# errors and robustness
+# ---------------------------------------------------------------------------------------
+
+def test_errors(pcc, ctx):
+    mb, om = model_pair(8, max_depth=12)
+    m = gpu_model(pcc, mb)
+    pts = I.random_cloud(500, 10, 2)
+    bs = O.encode(om, pts, 10)
+
+    def st(fn):
+        with pytest.raises(pcc.PCCError) as e:
+            fn()
+        return e.value.name
+
+    assert st(lambda: gpu_encode(pcc, ctx, m, [np.zeros((0, 3), np.int32)], 10)) == "EMPTY"
+    assert st(lambda: gpu_encode(pcc, ctx, m, [np.array([[0, 2000, 0]], np.int32)], 10)) == "RANGE"
+    assert st(lambda: gpu_encode(pcc, ctx, m, [pts], 13)) == "UNSUPPORTED_DEPTH"
+    assert st(lambda: gpu_decode(pcc, ctx, m, [b"XCC1" + bs[4:]], 600)) == "BAD_MAGIC"
+    assert st(lambda: gpu_decode(pcc, ctx, m, [bs[:4] + b"\x07\x00" + bs[6:]], 600)) == "VERSION"
+    other = gpu_model(pcc, model_pair(8, max_depth=12, seed=2)[0])
+    assert st(lambda: gpu_decode(pcc, ctx, other, [bs], 600)) == "MODEL_MISMATCH"
+    assert st(lambda: gpu_decode(pcc, ctx, m, [bs[:len(bs) - 8]], 600)) in ("TRUNCATED", "CORRUPT")
+    assert st(lambda: gpu_decode(pcc, ctx, m, [bs], 10)) == "CAPACITY"
+    rng = np.random.default_rng(7)
+    for _ in range(40):
+        d = bytearray(bs)
+        pos = int(rng.integers(24, len(d)))
+        d[pos] ^= 1 << int(rng.integers(0, 8))
+        try:
+            want = O.decode(om, bytes(d))[0]
+        except O.OracleError as e:
+            want = e.name
+        try:
+            got = gpu_decode(pcc, ctx, m, [bytes(d)], 4096)[0]
+        except pcc.PCCError as e:
+            got = e.name
+        if isinstance(want, str):
+            assert got in ("CORRUPT", "TRUNCATED"), (want, got)
+        else:
+            assert not isinstance(got, str) and np.array_equal(got, want)
+    # the context is still usable after errors
+    good, _ = gpu_encode(pcc, ctx, m, [pts], 10)
+    assert good[0] == bs
