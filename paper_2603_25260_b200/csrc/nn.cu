@@ -136,8 +136,12 @@ template <int C>
 __global__ void __launch_bounds__(128) k_down(const int8_t* __restrict__ g, const uint8_t* __restrict__ Xp,
                                               const uint32_t* __restrict__ cs, uint32_t np, const int8_t* __restrict__ W,
                                               const int32_t* __restrict__ bias, RQ rq, int8_t* __restrict__ out) {
-  __shared__ int32_t Ws[8 * C * C / 4];
-  for (int k = threadIdx.x; k < 8 * C * C / 4; k += blockDim.x) Ws[k] = reinterpret_cast<const int32_t*>(W)[k];
+  // per-child blocks padded by 4 words so lanes with different child index c read
+  // different banks
+  constexpr int CB = C * C / 4 + 4;
+  __shared__ int32_t Ws[8 * CB];
+  for (int k = threadIdx.x; k < 8 * C * C / 4; k += blockDim.x)
+    Ws[(k / (C * C / 4)) * CB + k % (C * C / 4)] = reinterpret_cast<const int32_t*>(W)[k];
   __syncthreads();
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > np) return;
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(128) k_down(const int8_t* __restrict__ g, cons
       int32_t v[C / 4];
       load_row<C / 4>(g + size_t(j) * C, v);
       ++j;
-      const int32_t* wr = Ws + c * C * (C / 4);
+      const int32_t* wr = Ws + c * CB;
 #pragma unroll
       for (int o = 0; o < C; ++o) {
         int32_t a = acc[o];
@@ -179,8 +183,12 @@ __global__ void __launch_bounds__(128) k_up(const int8_t* __restrict__ S, const 
                                             const uint32_t* __restrict__ par, const uint64_t* __restrict__ key_c,
                                             uint32_t nc, const int8_t* __restrict__ W, const int32_t* __restrict__ E,
                                             const int32_t* __restrict__ bias, RQ rq, int8_t* __restrict__ out) {
-  __shared__ int32_t Ws[8 * C * C / 4];
-  for (int k = threadIdx.x; k < 8 * C * C / 4; k += blockDim.x) Ws[k] = reinterpret_cast<const int32_t*>(W)[k];
+  // per-child blocks padded by 4 words so lanes with different child index c read
+  // different banks
+  constexpr int CB = C * C / 4 + 4;
+  __shared__ int32_t Ws[8 * CB];
+  for (int k = threadIdx.x; k < 8 * C * C / 4; k += blockDim.x)
+    Ws[(k / (C * C / 4)) * CB + k % (C * C / 4)] = reinterpret_cast<const int32_t*>(W)[k];
   __syncthreads();
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j > nc) return;
@@ -196,7 +204,7 @@ __global__ void __launch_bounds__(128) k_up(const int8_t* __restrict__ S, const 
     load_row<C / 4>(S + size_t(p) * C, v);
     const int32_t* er = E + size_t(x - 1) * (8 * C) + c * C;
     const int32_t* br = bias + c * C;
-    const int32_t* wr = Ws + c * C * (C / 4);
+    const int32_t* wr = Ws + c * CB;
 #pragma unroll
     for (int o = 0; o < C; ++o) {
       int32_t a = br[o] + er[o];

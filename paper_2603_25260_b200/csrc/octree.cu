@@ -395,13 +395,17 @@ uint32_t expand_level(pcc_ctx c, int d, int B, OctreeOut& o, uint32_t max_nodes)
   o.nb.resize(d + 3);
   o.nb[d + 2] = o.nb[d + 1] + nn;
   if (o.nb[d + 2] > c->bufs.at("key").cap / sizeof(uint64_t)) throw Error{PCC_ERR_CORRUPT};
-  Prof pe(c, "expand", size_t(n) * 13 + size_t(nn) * 12);
-  k_expand<<<cdiv(n, 256), 256, 0, s>>>(key_all + o.nb[d], code_all + o.nb[d], cs, n, key_all + o.nb[d + 1],
-                                        par_all + o.nb[d + 1]);
-  launched(c);
-  Prof pf(c, "expand", 0);
-  k_foff_next<<<cdiv(B + 1, 256), 256, 0, s>>>(cs, d_foff + size_t(d) * (B + 1), B, d_foff + size_t(d + 1) * (B + 1));
-  launched(c);
+  {
+    Prof pe(c, "expand", size_t(n) * 13 + size_t(nn) * 12);
+    k_expand<<<cdiv(n, 256), 256, 0, s>>>(key_all + o.nb[d], code_all + o.nb[d], cs, n, key_all + o.nb[d + 1],
+                                          par_all + o.nb[d + 1]);
+    launched(c);
+  }
+  {
+    Prof pf(c, "expand", 0);
+    k_foff_next<<<cdiv(B + 1, 256), 256, 0, s>>>(cs, d_foff + size_t(d) * (B + 1), B, d_foff + size_t(d + 1) * (B + 1));
+    launched(c);
+  }
   uint32_t* hf = static_cast<uint32_t*>(pinned(c, (B + 1) * sizeof(uint32_t)));
   PCC_CUDA(cudaMemcpyAsync(hf, d_foff + size_t(d + 1) * (B + 1), (B + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   PCC_CUDA(cudaStreamSynchronize(s));

@@ -198,7 +198,7 @@ struct DecSeg {
   uint32_t last;     // 1 if this is the level's last segment (must end the payload)
 };
 void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf, uint8_t* X,
-                 uint32_t* err);
+                 uint32_t* err, int max_lanes);
 
 // ---- pack (runtime.cu) ----
 struct PackItem {    // encoder output item: frame header+raw prefix (kind 0) or one segment (kind 1)

@@ -58,12 +58,17 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// Decoder: one warp per segment (block = 1 warp), CDF rows of the K nodes of the next
-// step prefetched into shared memory with cp.async (double buffer, 2 x 32 x 512 B).
+// Decoder: one warp per segment (block = 1 warp).  The CDF rows of the K nodes of a step
+// do not depend on the rANS state, so they are prefetched DEC_STAGES steps ahead into
+// shared memory with cp.async; the renormalisation words are consumed in stream order
+// and are held in a 96-word register window (three words per lane) refilled 64 words
+// ahead, so no step waits on a dependent global load.
+constexpr int DEC_STAGES = 4;
+
 __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs, int nseg, const uint8_t* __restrict__ bs,
                                                  const uint16_t* __restrict__ cdf, uint8_t* __restrict__ X,
-                                                 uint32_t* __restrict__ err) {
-  extern __shared__ __align__(16) uint16_t rows[];  // [2][32][256]
+                                                 uint32_t* __restrict__ err, int stage_rows) {
+  extern __shared__ __align__(16) uint16_t rows[];  // [DEC_STAGES][stage_rows][256]
   const int gw = blockIdx.x;
   const int lane = threadIdx.x;
   if (gw >= nseg) return;
@@ -92,39 +97,41 @@ __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs
       if (sg.last && pos + sz != lvl_bytes) bad = true;
     }
   }
-  if (bad) {
+  if (bad || K > stage_rows) {
     if (lane == 0) atomicOr(err, EF_CORRUPT);
     return;
   }
   uint32_t x = lane < K ? ld_u32(lvl + pos + 4 + 4 * lane) : (1u << 16);
   if (x < (1u << 16)) bad = true;
   const uint16_t* wp = reinterpret_cast<const uint16_t*>(lvl + pos + 4 + 4 * K);
+  auto ldw = [&](uint32_t k) -> uint32_t { return k < W ? uint32_t(wp[k]) : 0u; };
+  uint32_t wbase = 0;  // window = words [wbase, wbase + 96)
+  uint32_t w0 = ldw(lane), w1 = ldw(32 + lane), w2 = ldw(64 + lane);
   const uint32_t steps = (n + uint32_t(K) - 1u) / uint32_t(K);
   const uint16_t* base = cdf + size_t(sg.node) * 256;
   const unsigned lt = (1u << lane) - 1u;
   auto prefetch = [&](uint32_t s) {
-    uint16_t* buf = rows + (s & 1u) * (32 * 256);
-    for (int r = 0; r < K; ++r) {
-      const uint32_t j = s * uint32_t(K) + uint32_t(r);
-      if (j < n) cp_async16(buf + r * 256 + lane * 8, base + size_t(j) * 256 + lane * 8);
+    if (s < steps) {
+      uint16_t* buf = rows + size_t(s % DEC_STAGES) * stage_rows * 256;
+      for (int r = 0; r < K; ++r) {
+        const uint32_t j = s * uint32_t(K) + uint32_t(r);
+        if (j < n) cp_async16(buf + r * 256 + lane * 8, base + size_t(j) * 256 + lane * 8);
+      }
     }
-    cp_commit();
+    cp_commit();  // always commit (possibly empty) so group counting stays uniform
   };
-  prefetch(0);
+#pragma unroll
+  for (int p = 0; p < DEC_STAGES - 1; ++p) prefetch(uint32_t(p));
   uint32_t used = 0;
   for (uint32_t s = 0; s < steps; ++s) {
-    if (s + 1 < steps) {
-      prefetch(s + 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
+    prefetch(s + DEC_STAGES - 1);
+    cp_wait<DEC_STAGES - 1>();
     __syncwarp();
     const uint32_t j = s * uint32_t(K) + uint32_t(lane);
     const bool act = lane < K && j < n;
     bool need = false;
     if (act) {
-      const uint16_t* c = rows + (s & 1u) * (32 * 256) + lane * 256;
+      const uint16_t* c = rows + size_t(s % DEC_STAGES) * stage_rows * 256 + lane * 256;
       const uint32_t slot = x & 0xffffu;
       int lo = 0, hi = NCODE - 1;
 #pragma unroll
@@ -142,14 +149,24 @@ __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs
       need = x < (1u << 16);
     }
     const unsigned m = __ballot_sync(0xffffffffu, need);
+    const uint32_t off = used + __popc(m & lt) - wbase;  // < 64 + 32 since used - wbase < 32
+    const uint32_t v0 = __shfl_sync(0xffffffffu, w0, off & 31);
+    const uint32_t v1 = __shfl_sync(0xffffffffu, w1, off & 31);
+    const uint32_t v2 = __shfl_sync(0xffffffffu, w2, off & 31);
     if (need) {
-      const uint32_t wi = used + __popc(m & lt);
-      if (wi < W) x = (x << 16) | uint32_t(wp[wi]);
+      if (used + __popc(m & lt) < W) x = (x << 16) | (off < 32 ? v0 : (off < 64 ? v1 : v2));
       else bad = true;
     }
     used += __popc(m);
+    if (used - wbase >= 32) {  // slide the window by 32 words, load 64 ahead
+      wbase += 32;
+      w0 = w1;
+      w1 = w2;
+      w2 = ldw(wbase + 64 + lane);
+    }
     __syncwarp();
   }
+  cp_wait<0>();
   if (used != W || (lane < K && x != (1u << 16))) bad = true;
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, EF_CORRUPT);
 }
@@ -166,16 +183,18 @@ void rans_encode(pcc_ctx c, const EncSeg* d_segs, int nseg, const uint32_t* cf, 
 }
 
 void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf, uint8_t* X,
-                 uint32_t* err) {
+                 uint32_t* err, int max_lanes) {
   if (nseg == 0) return;
-  const size_t smem = 2 * 32 * 256 * sizeof(uint16_t);
+  const int stage_rows = max_lanes <= 8 ? 8 : (max_lanes <= 16 ? 16 : 32);
+  const size_t smem = size_t(DEC_STAGES) * stage_rows * 256 * sizeof(uint16_t);
   static bool attr = false;
   if (!attr) {
-    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(DEC_STAGES * 32 * 256 * sizeof(uint16_t))));
     attr = true;
   }
   Prof p(c, "rans_dec", 0);
-  k_rans_dec<<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, X, err);
+  k_rans_dec<<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, X, err, stage_rows);
   launched(c);
 }
 

@@ -772,12 +772,15 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
   if (o.nb[R + 1] > cap) throw Error{PCC_ERR_CORRUPT};
   PCC_CUDA(cudaMemcpyAsync(d_foff, upload(c, "foff_stage", o.foff), o.foff.size() * 4, cudaMemcpyDeviceToDevice, s));
   uint64_t* d_nb = upload(c, "nb", o.nb);
-  Prof praw(c, "container", 0);
-  k_raw_write<<<cdiv(B, 128), 128, 0, s>>>(d_bs, d_raw_off, B, R, d_foff, d_nb, static_cast<uint64_t*>(c->bufs.at("key").p),
-                                           static_cast<uint8_t*>(c->bufs.at("code").p),
-                                           static_cast<uint32_t*>(c->bufs.at("cs").p),
-                                           static_cast<uint32_t*>(c->bufs.at("par").p));
-  launched(c);
+  {
+    Prof praw(c, "container", 0);
+    k_raw_write<<<cdiv(B, 128), 128, 0, s>>>(d_bs, d_raw_off, B, R, d_foff, d_nb,
+                                             static_cast<uint64_t*>(c->bufs.at("key").p),
+                                             static_cast<uint8_t*>(c->bufs.at("code").p),
+                                             static_cast<uint32_t*>(c->bufs.at("cs").p),
+                                             static_cast<uint32_t*>(c->bufs.at("par").p));
+    launched(c);
+  }
   // 3. level-serial neural decoding (Eq.2)
   Net net{c, m, L, R, L - 1 - m->n_deep, C, o};
   std::vector<uint64_t> lvl_base(B);
@@ -803,7 +806,10 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
       lvl_base[f] += hd[f].lb[d - R];
     }
     DecSeg* d_segs = upload(c, "dsegs", segs);
-    rans_decode(c, d_segs, int(segs.size()), d_bs, cdf, static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d], err);
+    int kmax = 1;
+    for (const DecSeg& sg : segs) kmax = std::max(kmax, lanes_for(sg.n));
+    rans_decode(c, d_segs, int(segs.size()), d_bs, cdf, static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d], err,
+                kmax);
     PCC_CUDA(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s));
     PCC_CUDA(cudaStreamSynchronize(s));
     if (herr) throw Error{PCC_ERR_CORRUPT};
