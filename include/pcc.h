@@ -117,6 +117,10 @@ pcc_status pcc_decode_batch_host(pcc_ctx c, pcc_model m, const uint8_t* h_bs, co
  * "cf/l" (u16 pairs cum,freq; encode), "cdf/l" (u16 [N][256] cumulative; decode).
  * *len = bytes available; copies min(cap, len).  INVALID_ARG if unknown. */
 pcc_status pcc_debug_tensor(pcc_ctx c, const char* name, void* h_dst, size_t cap, size_t* len);
+/* Self-test of the tensor-core primitive used by the path (tcgen05.mma kind::i8,
+ * int32 accumulation in TMEM): h_d[128][n_cols] = h_a[128][32] * h_b[n_cols][32]^T,
+ * all HOST row-major int8/int32 arrays; n_cols in {32, 64, ..., 256}. */
+pcc_status pcc_debug_gemm_i8(pcc_ctx c, const int8_t* h_a, const int8_t* h_b, int n_cols, int32_t* h_d);
 /* Enable (1) / disable (0) retention of intermediate tensors for
  * pcc_debug_tensor (adds device->host copies; parity tests only). */
 pcc_status pcc_ctx_set_debug(pcc_ctx c, int on);

@@ -182,6 +182,11 @@ void up_prune(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* par
 void head_cdf(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
               const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg);
 
+// ---- head_tc.cu (tcgen05 kind::i8 predictor + softmax; same contract as head_cdf) ----
+void head_cdf_tc(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
+                 const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg);
+void gemm_i8_test(pcc_ctx c, const int8_t* dA, const int8_t* dB, int N, int32_t* dD);
+
 // ---- rans.cu ----
 struct EncSeg {      // one rANS segment of the encoder
   uint32_t node;     // first symbol (index into the concatenated cf / code arrays)

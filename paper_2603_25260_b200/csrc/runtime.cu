@@ -99,6 +99,19 @@ void dbg_copy(pcc_ctx c, const std::string& name, const void* dptr, size_t bytes
 namespace {
 
 inline unsigned cdiv(size_t a, size_t b) { return unsigned((a + b - 1) / b); }
+
+// Predictor + softmax: tcgen05 path by default; PCC_HEAD=simt selects the dp4a
+// warp-per-node kernel (kept as the A/B baseline; both are bit-exact).
+void head_any(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
+              const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg) {
+  static const bool simt = [] {
+    const char* e = getenv("PCC_HEAD");
+    return e && std::string(e) == "simt";
+  }();
+  if (simt) head_cdf(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
+  else head_cdf_tc(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
+}
+
 inline int lanes_for(uint32_t n) {
   uint32_t k = (n + 2047u) / 2048u;
   return int(k < 1u ? 1u : (k > 32u ? 32u : k));
@@ -582,7 +595,7 @@ void encode_batch(pcc_ctx c, pcc_model m, const int32_t* d_xyz, const size_t* of
   for (int d = R; d < L; ++d) {
     const int8_t* Fd = net.level(d);
     int8_t* a_dbg = c->debug ? buf<int8_t>(c, "t_adbg", size_t(o.N[d]) * m->H) : nullptr;
-    head_cdf(c, Fd, o.N[d], C, m->H, net.head_of(d), m->lut, 0, net.X(d), cf + o.nb[d], nullptr, a_dbg);
+    head_any(c, Fd, o.N[d], C, m->H, net.head_of(d), m->lut, 0, net.X(d), cf + o.nb[d], nullptr, a_dbg);
     if (c->debug) {
       dbg_copy(c, nm("a", d), a_dbg, size_t(o.N[d]) * m->H);
       dbg_copy(c, nm("cf", d), cf + o.nb[d], size_t(o.N[d]) * 4);
@@ -790,7 +803,7 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
     const uint32_t nd = o.N[d];
     uint16_t* cdf = buf<uint16_t>(c, "cdf", size_t(nd) * 256);
     int8_t* a_dbg = c->debug ? buf<int8_t>(c, "t_adbg", size_t(nd) * m->H) : nullptr;
-    head_cdf(c, Fd, nd, C, m->H, net.head_of(d), m->lut, 1, nullptr, nullptr, cdf, a_dbg);
+    head_any(c, Fd, nd, C, m->H, net.head_of(d), m->lut, 1, nullptr, nullptr, cdf, a_dbg);
     if (c->debug) {
       dbg_copy(c, nm("a", d), a_dbg, size_t(nd) * m->H);
       dbg_copy(c, nm("cdf", d), cdf, size_t(nd) * 512);
@@ -1041,6 +1054,22 @@ pcc_status pcc_debug_tensor(pcc_ctx c, const char* name, void* h_dst, size_t cap
   *len = it->second.size();
   if (h_dst) std::memcpy(h_dst, it->second.data(), std::min(cap, it->second.size()));
   return PCC_OK;
+}
+
+pcc_status pcc_debug_gemm_i8(pcc_ctx c, const int8_t* h_a, const int8_t* h_b, int n_cols, int32_t* h_d) {
+  if (!c || !h_a || !h_b || !h_d) return PCC_ERR_INVALID_ARG;
+  return guard(c, [&] {
+    PCC_CUDA(cudaSetDevice(c->device));
+    int8_t* dA = wsT<int8_t>(c, "gt_a", 128 * 32);
+    int8_t* dB = wsT<int8_t>(c, "gt_b", size_t(n_cols) * 32);
+    int32_t* dD = wsT<int32_t>(c, "gt_d", size_t(128) * n_cols);
+    PCC_CUDA(cudaMemcpyAsync(dA, h_a, 128 * 32, cudaMemcpyHostToDevice, c->stream));
+    PCC_CUDA(cudaMemcpyAsync(dB, h_b, size_t(n_cols) * 32, cudaMemcpyHostToDevice, c->stream));
+    gemm_i8_test(c, dA, dB, n_cols, dD);
+    PCC_CUDA(cudaMemcpyAsync(h_d, dD, size_t(128) * n_cols * 4, cudaMemcpyDeviceToHost, c->stream));
+    PCC_CUDA(cudaStreamSynchronize(c->stream));
+    PCC_CUDA(cudaGetLastError());
+  });
 }
 
 pcc_status pcc_ctx_set_debug(pcc_ctx c, int on) {

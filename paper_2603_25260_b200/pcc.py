@@ -60,6 +60,8 @@ def _load():
     L.pcc_ctx_profile_get.restype = I
     L.pcc_ctx_profile_categories.argtypes = [P]
     L.pcc_ctx_profile_categories.restype = ct.c_char_p
+    L.pcc_debug_gemm_i8.argtypes = [P, P, P, I, P]
+    L.pcc_debug_gemm_i8.restype = I
     L.pcc_status_string.argtypes = [I]
     L.pcc_status_string.restype = ct.c_char_p
     for f in ("pcc_model_load", "pcc_model_hash", "pcc_model_info", "pcc_ctx_create", "pcc_build_octree",
@@ -75,7 +77,7 @@ EXPORTS = ("pcc_model_load", "pcc_model_hash", "pcc_model_info", "pcc_model_dest
            "pcc_ctx_destroy", "pcc_encode_bound", "pcc_build_octree", "pcc_encode", "pcc_decode",
            "pcc_encode_batch", "pcc_decode_batch", "pcc_encode_batch_host", "pcc_decode_batch_host",
            "pcc_debug_tensor", "pcc_ctx_set_debug", "pcc_ctx_launch_count", "pcc_ctx_set_profile",
-           "pcc_ctx_profile_get", "pcc_ctx_profile_categories", "pcc_status_string")
+           "pcc_ctx_profile_get", "pcc_ctx_profile_categories", "pcc_debug_gemm_i8", "pcc_status_string")
 
 
 def _ptr(x) -> Optional[int]:
@@ -222,6 +224,16 @@ def pcc_ctx_profile_get(ctx, category: Optional[str] = None) -> Tuple[float, int
 
 def pcc_ctx_profile_categories(ctx) -> list:
     return lib.pcc_ctx_profile_categories(ctx).decode().split()
+
+
+def pcc_debug_gemm_i8(ctx, a, b):
+    """a: int8 numpy [128, 32], b: int8 numpy [N, 32] -> int32 numpy [128, N] via tcgen05."""
+    import numpy as np
+    a = np.ascontiguousarray(a, np.int8)
+    b = np.ascontiguousarray(b, np.int8)
+    d = np.zeros((128, b.shape[0]), np.int32)
+    _chk(lib.pcc_debug_gemm_i8(ctx, a.ctypes.data, b.ctypes.data, b.shape[0], d.ctypes.data), "pcc_debug_gemm_i8")
+    return d
 
 
 def pcc_status_string(st: int) -> str:

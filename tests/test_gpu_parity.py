@@ -89,6 +89,21 @@ def morton_sorted_unique(pts, L):
 
 
 # ---------------------------------------------------------------------------------------
+# tensor-core primitive (tcgen05.mma kind::i8, TMEM int32 accumulators)
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("N", [32, 64, 256])
+def test_tcgen05_int8_gemm(pcc, ctx, N):
+    rng = np.random.default_rng(N)
+    a = rng.integers(-128, 128, size=(128, 32)).astype(np.int8)
+    b = rng.integers(-128, 128, size=(N, 32)).astype(np.int8)
+    a[0] = -128
+    b[0] = -128   # extreme corner: 32 * 2^14 = 2^19
+    d = pcc.pcc_debug_gemm_i8(ctx, a, b)
+    assert np.array_equal(d, a.astype(np.int64) @ b.astype(np.int64).T)
+
+
+# ---------------------------------------------------------------------------------------
 # octree (a1, a2)
 # ---------------------------------------------------------------------------------------
 
