@@ -62,7 +62,7 @@ struct SmemLayout {
   static constexpr int ROWI = 18704;    // 128 x (left, istar)
   static constexpr int STAGE = 19776;   // decoder: 128 x STG u16
   static constexpr int END_DEC = STAGE + TILE * STG * 2;
-  static constexpr int END = 80 * 1024; // >= END_DEC; caps residency at 2 CTAs/SM (TMEM: 2 x 256 cols)
+  static constexpr int END = 88 * 1024; // >= END_DEC; caps residency at 2 CTAs/SM (TMEM: 2 x 256 cols)
 };
 static_assert(SmemLayout::END_DEC <= SmemLayout::END, "decoder staging exceeds the smem budget");
 
