@@ -512,9 +512,10 @@ void cdf_quantize(const int32_t* z, const RQ& rql, const std::vector<uint32_t>& 
 
 // ---- rANS (reading O9/O10/Q23/Q24) ---------------------------------------------
 // 32-bit state, L = 2^16, 16-bit words, M = 2^16.  Symbol j of a segment of n goes to
-// lane j mod K at step j / K with K = clamp(ceil(n/2048), 1, 32).
+// lane j mod K at step j / K with K = clamp(ceil(n/512), 1, 32) (segments of 16384 symbols:
+// at most 512 sequential steps per lane, reading Q24).
 int lanes_for(size_t n) {
-  size_t k = (n + 2047) / 2048;
+  size_t k = (n + 511) / 512;
   if (k < 1) k = 1;
   if (k > 32) k = 32;
   return int(k);
@@ -698,7 +699,7 @@ struct Coder {
 //                u16 raw_bytes | u32 N_L | u64 model_hash
 // u32 level_bytes[L-R]; raw prefix X_0..X_{R-1} (raw_bytes, zero-padded to 4);
 // level payloads d = R..L-1 (each a sequence of 4-byte-aligned rANS segments).
-constexpr size_t SEG = 65536;
+constexpr size_t SEG = 16384;
 
 void check_depth(const Model& m, int L) {
   if (L < m.R + 1 + m.n_deep || L < m.min_depth || L > m.max_depth || L > 21) throw Fail{UNSUPPORTED_DEPTH};

@@ -13,7 +13,7 @@
 namespace pcc {
 
 constexpr int NCODE = 255;     // occupancy classes
-constexpr int SEG_SYMS = 65536; // rANS segment length (reading Q24)
+constexpr int SEG_SYMS = 16384; // rANS segment length (reading Q24: <= 512 steps per lane)
 constexpr int MAX_LANES = 32;
 constexpr int MAX_DEPTH = 21;   // 63-bit Morton key cap
 

@@ -10,7 +10,7 @@ namespace pcc {
 namespace {
 
 __device__ __forceinline__ int lanes_for(uint32_t n) {
-  uint32_t k = (n + 2047u) / 2048u;
+  uint32_t k = (n + 511u) / 512u;
   return int(k < 1u ? 1u : (k > 32u ? 32u : k));
 }
 
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs
   const DecSeg sg = segs[gw];
   const uint8_t* lvl = bs + sg.byte;
   const uint32_t lvl_bytes = sg.level_bytes;
-  // walk earlier (full, 65536-symbol, K = 32) chunks of this level payload
+  // walk earlier (full, 16384-symbol, K = 32) chunks of this level payload
   uint32_t pos = 0;
   bool bad = false;
   for (uint32_t ch = 0; ch < sg.chunk && !bad; ++ch) {

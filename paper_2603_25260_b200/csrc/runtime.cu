@@ -113,7 +113,7 @@ void head_any(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead&
 }
 
 inline int lanes_for(uint32_t n) {
-  uint32_t k = (n + 2047u) / 2048u;
+  uint32_t k = (n + 511u) / 512u;
   return int(k < 1u ? 1u : (k > 32u ? 32u : k));
 }
 
@@ -428,7 +428,7 @@ __global__ void k_pack_sizes(const PackItem* __restrict__ items, int n, const En
     sizes[i] = it.bytes;
   } else {
     const uint32_t ns = segs[it.seg].n;
-    uint32_t k = (ns + 2047u) / 2048u;
+    uint32_t k = (ns + 511u) / 512u;
     k = k < 1u ? 1u : (k > 32u ? 32u : k);
     sizes[i] = 4u + 4u * k + 4u * ((seg_W[it.seg] + 1u) / 2u);
   }
@@ -478,7 +478,7 @@ __global__ void k_pack_write(const PackItem* __restrict__ items, int n, const ui
   } else {
     const EncSeg sg = segs[it.seg];
     const uint32_t W = seg_W[it.seg];
-    uint32_t K = (sg.n + 2047u) / 2048u;
+    uint32_t K = (sg.n + 511u) / 512u;
     K = K < 1u ? 1u : (K > 32u ? 32u : K);
     uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
     if (lane == 0) o32[0] = W;

@@ -246,7 +246,7 @@ def test_zero_model_and_max_depth(pcc, ctx):
 
 
 def test_large_level_multi_segment(pcc, ctx):
-    """A level with > 65536 nodes spans several rANS segments (reading Q24)."""
+    """A level with > 16384 nodes spans several rANS segments (reading Q24)."""
     mb, om = model_pair(8, max_depth=12)
     m = gpu_model(pcc, mb)
     pts = I.random_cloud(150000, 12, 21)

@@ -60,8 +60,8 @@ def _payload_bits(level_bytes, N):
     """Bits of rANS words in a level payload (segment headers/states excluded) and lane count."""
     bits, lanes, pos, left = 0, 0, 0, N
     while left > 0:
-        n = min(65536, left)
-        K = min(32, max(1, -(-n // 2048)))
+        n = min(16384, left)
+        K = min(32, max(1, -(-n // 512)))
         W = struct.unpack_from("<I", level_bytes, pos)[0]
         bits += 16 * W
         lanes += K
@@ -111,7 +111,7 @@ def test_zero_model_closed_form_length():
         n1 = int((codes[d] == 1).sum())
         ideal = n1 * math.log2(65536 / 258) + (codes[d].size - n1) * math.log2(65536 / 257)
         bits, K = _payload_bits(levels[d], codes[d].size)
-        assert ideal * 0.98 - 32 <= bits <= ideal * 1.002 + 16 * K, d
+        assert ideal * 0.98 - 16 * K - 16 <= bits <= ideal * 1.002 + 16 * K, d
 
 
 def test_bias_only_head_length():
@@ -127,7 +127,7 @@ def test_bias_only_head_length():
         hist = np.bincount(codes[d], minlength=256)[1:]
         ideal = float(np.sum(hist * np.log2(65536.0 / p)))
         bits, K = _payload_bits(levels[d], codes[d].size)
-        assert ideal * 0.98 - 32 <= bits <= ideal * 1.002 + 16 * K, d
+        assert ideal * 0.98 - 16 * K - 16 <= bits <= ideal * 1.002 + 16 * K, d
 
 
 def test_length_matches_pmf_dumps(model):
@@ -139,7 +139,7 @@ def test_length_matches_pmf_dumps(model):
         x = D.get(f"code/{d}", np.uint8).astype(np.int64)
         ideal = float(np.sum(np.log2(65536.0 / p[np.arange(x.size), x - 1])))
         bits, K = _payload_bits(levels[d], x.size)
-        assert ideal * 0.98 - 32 <= bits <= ideal * 1.002 + 16 * K, d
+        assert ideal * 0.98 - 16 * K - 16 <= bits <= ideal * 1.002 + 16 * K, d
         # pmf rows are valid Q16 distributions
         assert np.all(p.sum(1) == 65536) and p.min() >= 1
 
