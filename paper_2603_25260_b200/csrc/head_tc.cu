@@ -1,13 +1,13 @@
 // head_tc.cu — occupancy predictor (Eq.7) + integer softmax to a Q16 pmf
 // (Eq.15; readings Q20-Q22) on the 5th-generation tensor cores.
 //
-// One CTA = 128 threads = one 128-node tile per iteration (persistent over tiles).
+// One CTA = 512 threads = one 128-node tile per iteration (persistent over tiles).
 //   1. hidden layer a = prq(W1 F + b1) (C -> H, int8 dp4a) written straight into the
 //      tcgen05 A operand (canonical K-major smem tile, K padded to 32 with zeros);
 //   2. z = a W2^T: ONE tcgen05.mma.kind::i8 (M = 128, N = 256, K = 32) into TMEM
 //      (int32; column 255 is padding);
-//   3. thread t owns TMEM lane t = node t of the tile and runs the softmax over its
-//      row with 32-column tcgen05.ld loads: pass 1 requantises z to Q8 logits (written
+//   3. four threads own TMEM lane r = node r of the tile (one 64-column quarter each)
+//      and run the softmax over the row with 16-column tcgen05.ld loads: pass 1 requantises z to Q8 logits (written
 //      back with tcgen05.st) and finds max / first argmax, pass 2 turns them into LUT
 //      exponentials (written back) and their sum S, pass 3 forms p = 1 + floor(e*65281/S)
 //      (exact: 64-bit reciprocal + one integer correction) and either the (cum, freq)
@@ -50,6 +50,26 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+
+// 512 threads per CTA: 16 warps.  Warp w may only touch TMEM lanes 32*(w%4)..+31, so
+// thread t owns row r = 32*(w%4) + t%32 of the tile and column quarter q = w/4
+// (columns 64q..64q+63); the 4 threads of a row combine max / sum / totals in smem.
+constexpr int NT = 512;
 struct SmemLayout {
   static constexpr int B = 0;           // W2 operand 256 x 32 (8 KB)
   static constexpr int A = 8192;        // a operand 128 x 32 (4 KB)
@@ -59,20 +79,19 @@ struct SmemLayout {
   static constexpr int B1 = 18432;      // <= 256 B
   static constexpr int MBAR = 18688;
   static constexpr int THOLD = 18696;
-  static constexpr int ROWI = 18704;    // 128 x (left, istar)
-  static constexpr int STAGE = 19776;   // decoder: 128 x STG u16
-  static constexpr int END_DEC = STAGE + TILE * STG * 2;
-  static constexpr int END = 88 * 1024; // >= END_DEC; caps residency at 2 CTAs/SM (TMEM: 2 x 256 cols)
+  static constexpr int RED = 18704;     // [4][128] x (a, b) int32 = 4 KB
+  static constexpr int ROWI = 22800;    // [128] x 8 int32 = 4 KB
+  static constexpr int STAGE = 26896;   // decoder: 128 x STG u16 (66 KB)
+  static constexpr int END = STAGE + TILE * STG * 2;
 };
-static_assert(SmemLayout::END_DEC <= SmemLayout::END, "decoder staging exceeds the smem budget");
 
 template <int C, int H, int MODE>
-__global__ void __launch_bounds__(TILE, 2) k_head_tc(const int8_t* __restrict__ F, uint32_t n,
-                                                     const int8_t* __restrict__ W1, const int32_t* __restrict__ b1, RQ rq1,
-                                                     const int8_t* __restrict__ W2, const int32_t* __restrict__ b2, RQ rql,
-                                                     const uint32_t* __restrict__ lut, const uint8_t* __restrict__ X,
-                                                     uint32_t* __restrict__ cf, uint16_t* __restrict__ cdf,
-                                                     int8_t* __restrict__ a_dbg) {
+__global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F, uint32_t n,
+                                                   const int8_t* __restrict__ W1, const int32_t* __restrict__ b1, RQ rq1,
+                                                   const int8_t* __restrict__ W2, const int32_t* __restrict__ b2, RQ rql,
+                                                   const uint32_t* __restrict__ lut, const uint8_t* __restrict__ X,
+                                                   uint32_t* __restrict__ cf, uint16_t* __restrict__ cdf,
+                                                   int8_t* __restrict__ a_dbg) {
   extern __shared__ __align__(1024) uint8_t sm[];
   using S = SmemLayout;
   uint8_t* sB = sm + S::B;
@@ -83,21 +102,24 @@ __global__ void __launch_bounds__(TILE, 2) k_head_tc(const int8_t* __restrict__ 
   int32_t* sb1 = reinterpret_cast<int32_t*>(sm + S::B1);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + S::MBAR);
   uint32_t* thold = reinterpret_cast<uint32_t*>(sm + S::THOLD);
-  int32_t* rowi = reinterpret_cast<int32_t*>(sm + S::ROWI);
+  int32_t* red = reinterpret_cast<int32_t*>(sm + S::RED);    // red[(q*128 + r)*2 + {0,1}]
+  int32_t* rowi = reinterpret_cast<int32_t*>(sm + S::ROWI);  // rowi[r*8 + k]
   uint16_t* stage = reinterpret_cast<uint16_t*>(sm + S::STAGE);
   const int tid = threadIdx.x, warp = tid >> 5;
-  constexpr int CW = C / 4, HW = H / 4;
+  const int r = 32 * (warp & 3) + (tid & 31);  // row of the tile (= TMEM lane)
+  const int q = warp >> 2;                     // column quarter
+  constexpr int CW = C / 4, HW = H / 4, HQ = H / 4;  // HQ hidden units per thread
 
-  // B operand: W2 [256][H] -> canonical K-major 256 x 32 (K >= H zero-padded)
-  for (int k = tid; k < 256 * 8; k += TILE) {
-    const int r = k >> 3, w = k & 7;
-    const uint32_t v = (w < HW) ? reinterpret_cast<const uint32_t*>(W2)[r * HW + w] : 0u;
-    *reinterpret_cast<uint32_t*>(sB + tc::kmaj_off(r, 4 * w)) = v;
+  for (int k = tid; k < 256 * 8; k += NT) {
+    const int rr = k >> 3, w = k & 7;
+    const uint32_t v = (w < HW) ? reinterpret_cast<const uint32_t*>(W2)[rr * HW + w] : 0u;
+    *reinterpret_cast<uint32_t*>(sB + tc::kmaj_off(rr, 4 * w)) = v;
   }
-  for (int k = tid; k < 1024; k += TILE) sLut[k] = lut[k];
-  for (int k = tid; k < 256; k += TILE) sb2[k] = b2[k];
-  for (int k = tid; k < H * CW; k += TILE) sW1[k] = reinterpret_cast<const int32_t*>(W1)[k];
-  for (int k = tid; k < H; k += TILE) sb1[k] = b1[k];
+  for (int k = tid; k < 1024; k += NT) reinterpret_cast<uint32_t*>(sA)[k] = 0u;  // K padding stays 0
+  for (int k = tid; k < 1024; k += NT) sLut[k] = lut[k];
+  for (int k = tid; k < 256; k += NT) sb2[k] = b2[k];
+  for (int k = tid; k < H * CW; k += NT) sW1[k] = reinterpret_cast<const int32_t*>(W1)[k];
+  for (int k = tid; k < H; k += NT) sb1[k] = b1[k];
   if (warp == 0) tc::tmem_alloc<256>(thold);
   if (tid == 0) tc::mbar_init(mbar, 1);
   tc::fence_async_smem();
@@ -105,36 +127,39 @@ __global__ void __launch_bounds__(TILE, 2) k_head_tc(const int8_t* __restrict__ 
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = *thold;
-  const uint32_t taddr = tbase + (uint32_t(warp * 32) << 16);
+  const uint32_t taddr = tbase + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(64 * q);
   const uint64_t adesc = tc::sdesc(tc::smem_u32(sA));
   const uint64_t bdesc = tc::sdesc(tc::smem_u32(sB));
   const uint32_t ntiles = (n + TILE - 1) / TILE;
   uint32_t phase = 0;
 
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t row = tile * TILE + tid;
+    const uint32_t row = tile * TILE + r;
     const bool valid = row < n;
-    // ---- hidden layer (C -> H) into the A operand ----
-    int32_t fw[CW];
+    // ---- hidden layer: this thread's H/4 units of row r, into the A operand ----
+    {
+      int32_t fw[CW];
 #pragma unroll
-    for (int w = 0; w < CW; ++w) fw[w] = valid ? reinterpret_cast<const int32_t*>(F + size_t(row) * C)[w] : 0;
-    uint32_t aw[8];
+      for (int w = 0; w < CW; ++w) fw[w] = valid ? reinterpret_cast<const int32_t*>(F + size_t(row) * C)[w] : 0;
+      uint32_t ab[2] = {0u, 0u};
 #pragma unroll
-    for (int w = 0; w < 8; ++w) aw[w] = 0;
+      for (int hh = 0; hh < HQ; ++hh) {
+        const int h = q * HQ + hh;
+        int32_t acc = sb1[h];
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
-      int32_t acc = sb1[h];
+        for (int w = 0; w < CW; ++w) acc = __dp4a(fw[w], sW1[h * CW + w], acc);
+        ab[hh >> 2] |= (uint32_t(rq8(acc, rq1)) & 0xffu) << (8 * (hh & 3));
+      }
+      uint8_t* dst = sA + tc::kmaj_off(r, q * HQ);
+      if constexpr (HQ == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(ab[0], ab[1]);
+      else if constexpr (HQ == 4) *reinterpret_cast<uint32_t*>(dst) = ab[0];
+      else *reinterpret_cast<uint16_t*>(dst) = uint16_t(ab[0]);
+      if (a_dbg && valid) {
+        int8_t* ad = a_dbg + size_t(row) * H + q * HQ;
 #pragma unroll
-      for (int w = 0; w < CW; ++w) acc = __dp4a(fw[w], sW1[h * CW + w], acc);
-      const uint32_t q = uint32_t(rq8(acc, rq1)) & 0xffu;
-      aw[h >> 2] |= q << (8 * (h & 3));
+        for (int hh = 0; hh < HQ; ++hh) ad[hh] = int8_t(ab[hh >> 2] >> (8 * (hh & 3)));
+      }
     }
-    if (a_dbg && valid) {
-#pragma unroll
-      for (int w = 0; w < HW; ++w) reinterpret_cast<uint32_t*>(a_dbg + size_t(row) * H)[w] = aw[w];
-    }
-    *reinterpret_cast<uint4*>(sA + tc::kmaj_off(tid, 0)) = make_uint4(aw[0], aw[1], aw[2], aw[3]);
-    *reinterpret_cast<uint4*>(sA + tc::kmaj_off(tid, 16)) = make_uint4(aw[4], aw[5], aw[6], aw[7]);
     tc::fence_async_smem();
     tc::fence_before();
     __syncthreads();
@@ -147,115 +172,157 @@ __global__ void __launch_bounds__(TILE, 2) k_head_tc(const int8_t* __restrict__ 
     phase ^= 1u;
     tc::fence_after();
 
-    // ---- pass 1: Q8 logits (stored back into TMEM), max and first argmax ----
+    // ---- pass 1: Q8 logits (back into TMEM), local max / first argmax ----
     int32_t lmax = INT32_MIN;
-    int istar = 0;
+    int ist = 1 << 30;
 #pragma unroll 1
-    for (int ch = 0; ch < 8; ++ch) {
-      uint32_t v[32];
-      tc::tmem_ld32(taddr + ch * 32, v);
+    for (int ch = 0; ch < 4; ++ch) {
+      uint32_t v[16];
+      tmem_ld16(taddr + ch * 16, v);
       tc::tmem_wait_ld();
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const int i = ch * 32 + k;
+      for (int k = 0; k < 16; ++k) {
+        const int i = 64 * q + ch * 16 + k;
         const int32_t l = lq8(int32_t(v[k]) + sb2[i], rql);
         v[k] = uint32_t(l);
         if (i < NCODE && l > lmax) {
           lmax = l;
-          istar = i;
+          ist = i;
         }
       }
-      tmem_st32(taddr + ch * 32, v);
+      tmem_st16(taddr + ch * 16, v);
     }
+    red[(q * TILE + r) * 2] = lmax;
+    red[(q * TILE + r) * 2 + 1] = ist;
+    __syncthreads();
+    int32_t mu = red[r * 2];
+    for (int qq = 1; qq < 4; ++qq) mu = max(mu, red[(qq * TILE + r) * 2]);
+    int istar = 1 << 30;
+    for (int qq = 3; qq >= 0; --qq)
+      if (red[(qq * TILE + r) * 2] == mu) istar = red[(qq * TILE + r) * 2 + 1];
     tmem_wait_st();
-    // ---- pass 2: e = LUT[delta >> 2] (0 beyond 16 nats), S = sum e ----
-    uint32_t Ssum = 0;
+    // ---- pass 2: e = LUT[delta >> 2] (0 beyond 16 nats), local sum ----
+    uint32_t ssum = 0;
 #pragma unroll 1
-    for (int ch = 0; ch < 8; ++ch) {
-      uint32_t v[32];
-      tc::tmem_ld32(taddr + ch * 32, v);
+    for (int ch = 0; ch < 4; ++ch) {
+      uint32_t v[16];
+      tmem_ld16(taddr + ch * 16, v);
       tc::tmem_wait_ld();
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const int i = ch * 32 + k;
-        const uint32_t dl = uint32_t(lmax - int32_t(v[k]));
+      for (int k = 0; k < 16; ++k) {
+        const int i = 64 * q + ch * 16 + k;
+        const uint32_t dl = uint32_t(mu - int32_t(v[k]));
         const uint32_t e = (i < NCODE && dl < 4096u) ? sLut[dl >> 2] : 0u;
         v[k] = e;
-        Ssum += e;
+        ssum += e;
       }
-      tmem_st32(taddr + ch * 32, v);
+      tmem_st16(taddr + ch * 16, v);
     }
+    __syncthreads();  // everyone has read red (pass-1 values) before it is overwritten
+    red[(q * TILE + r) * 2] = int32_t(ssum);
+    __syncthreads();
+    const uint32_t Ssum = uint32_t(red[r * 2]) + uint32_t(red[(TILE + r) * 2]) + uint32_t(red[(2 * TILE + r) * 2]) +
+                          uint32_t(red[(3 * TILE + r) * 2]);
     tmem_wait_st();
-    // ---- pass 3: p = 1 + floor(e * 65281 / S), leftover to the first argmax ----
+    // ---- pass 3: p = 1 + floor(e * 65281 / S) (exact), leftover to the first argmax ----
     const uint64_t inv = ~0ull / uint64_t(Ssum);
     uint32_t tot = 0;
     if constexpr (MODE == 0) {
       const int sym = valid ? int(X[row]) - 1 : 0;
       uint32_t cum = 0, fq = 0;
 #pragma unroll 1
-      for (int ch = 0; ch < 8; ++ch) {
-        uint32_t v[32];
-        tc::tmem_ld32(taddr + ch * 32, v);
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t v[16];
+        tmem_ld16(taddr + ch * 16, v);
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const int i = ch * 32 + k;
+        for (int k = 0; k < 16; ++k) {
+          const int i = 64 * q + ch * 16 + k;
           const uint64_t num = uint64_t(v[k]) * 65281ull;
-          uint64_t q = __umul64hi(num, inv);
-          if (num - q * uint64_t(Ssum) >= uint64_t(Ssum)) ++q;
-          const uint32_t p = (i < NCODE) ? uint32_t(1 + q) : 0u;
+          uint64_t qt = __umul64hi(num, inv);
+          if (num - qt * uint64_t(Ssum) >= uint64_t(Ssum)) ++qt;
+          const uint32_t p = (i < NCODE) ? uint32_t(1 + qt) : 0u;
           tot += p;
           cum += (i < sym) ? p : 0u;
           fq = (i == sym) ? p : fq;
         }
       }
-      const uint32_t left = 65536u - tot;
-      if (istar < sym) cum += left;
-      if (istar == sym) fq += left;
-      if (valid) cf[row] = cum | (fq << 16);
+      __syncthreads();  // Ssum reads done
+      red[(q * TILE + r) * 2] = int32_t(tot);
+      red[(q * TILE + r) * 2 + 1] = int32_t(cum | (fq << 16));  // cum < 2^16 per quarter? use rowi
+      rowi[r * 8 + q] = int32_t(cum);
+      rowi[r * 8 + 4 + q] = int32_t(fq);
+      __syncthreads();
+      if (q == 0 && valid) {
+        uint32_t T = 0, cm = 0, f = 0;
+        for (int qq = 0; qq < 4; ++qq) {
+          T += uint32_t(red[(qq * TILE + r) * 2]);
+          cm += uint32_t(rowi[r * 8 + qq]);
+          f += uint32_t(rowi[r * 8 + 4 + qq]);
+        }
+        const uint32_t left = 65536u - T;
+        if (istar < sym) cm += left;
+        if (istar == sym) f += left;
+        cf[row] = cm | (f << 16);
+      }
     } else {
-      uint16_t* srow = stage + tid * STG;
+      uint16_t* srow = stage + r * STG;
       uint32_t run = 0;
 #pragma unroll 1
-      for (int ch = 0; ch < 8; ++ch) {
-        uint32_t v[32];
-        tc::tmem_ld32(taddr + ch * 32, v);
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t v[16];
+        tmem_ld16(taddr + ch * 16, v);
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          const int i = ch * 32 + k;
+        for (int k = 0; k < 16; k += 2) {
+          const int i = 64 * q + ch * 16 + k;
           uint32_t c2[2];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const uint64_t num = uint64_t(v[k + u]) * 65281ull;
-            uint64_t q = __umul64hi(num, inv);
-            if (num - q * uint64_t(Ssum) >= uint64_t(Ssum)) ++q;
-            const uint32_t p = (i + u < NCODE) ? uint32_t(1 + q) : 0u;
-            c2[u] = run;
+            uint64_t qt = __umul64hi(num, inv);
+            if (num - qt * uint64_t(Ssum) >= uint64_t(Ssum)) ++qt;
+            const uint32_t p = (i + u < NCODE) ? uint32_t(1 + qt) : 0u;
+            c2[u] = run;  // quarter-local prefix (< 2^16)
             run += p;
           }
           *reinterpret_cast<uint32_t*>(srow + i) = (c2[0] & 0xffffu) | (c2[1] << 16);
         }
       }
-      tot = run;
-      rowi[2 * tid] = int32_t(65536u - tot);
-      rowi[2 * tid + 1] = istar;
+      __syncthreads();  // Ssum reads done
+      red[(q * TILE + r) * 2] = int32_t(run);
       __syncthreads();
-      // coalesced write-out: one 512-byte row per iteration, leftover added after i*
+      if (q == 0) {
+        uint32_t o = 0;
+        for (int qq = 0; qq < 4; ++qq) {
+          rowi[r * 8 + qq] = int32_t(o);  // prefix of the quarter totals
+          o += uint32_t(red[(qq * TILE + r) * 2]);
+        }
+        rowi[r * 8 + 4] = int32_t(65536u - o);  // leftover
+        rowi[r * 8 + 5] = istar;
+      }
+      __syncthreads();
+      // coalesced write-out: 4 rows per iteration, 128 u16 pairs per row
       const uint32_t rows_here = (n - tile * TILE) < uint32_t(TILE) ? (n - tile * TILE) : uint32_t(TILE);
-      for (uint32_t r = 0; r < rows_here; ++r) {
-        const uint32_t i0 = 2u * tid;
-        const uint32_t left = uint32_t(rowi[2 * r]);
-        const int ist = rowi[2 * r + 1];
-        const uint32_t pair = *reinterpret_cast<const uint32_t*>(stage + r * STG + i0);
-        uint32_t c0 = (pair & 0xffffu) + (int(i0) > ist ? left : 0u);
-        uint32_t c1 = (pair >> 16) + (int(i0 + 1) > ist ? left : 0u);
-        if (i0 + 1 >= uint32_t(NCODE)) c1 = 0xffffu;
-        reinterpret_cast<uint32_t*>(cdf + size_t(tile * TILE + r) * 256)[tid] = (c0 & 0xffffu) | (c1 << 16);
+      const uint32_t pr = uint32_t(tid) & 127u, sub = uint32_t(tid) >> 7;
+      for (uint32_t rb = 0; rb < rows_here; rb += 4) {
+        const uint32_t rr = rb + sub;
+        if (rr < rows_here) {
+          const uint32_t i0 = 2u * pr;
+          const int32_t* ri = rowi + rr * 8;
+          const uint32_t off = uint32_t(ri[i0 >> 6]);
+          const uint32_t left = uint32_t(ri[4]);
+          const int isr = ri[5];
+          const uint32_t pair = *reinterpret_cast<const uint32_t*>(stage + rr * STG + i0);
+          const uint32_t c0 = (pair & 0xffffu) + off + (int(i0) > isr ? left : 0u);
+          uint32_t c1 = (pair >> 16) + off + (int(i0 + 1) > isr ? left : 0u);
+          if (i0 + 1 >= uint32_t(NCODE)) c1 = 0xffffu;
+          reinterpret_cast<uint32_t*>(cdf + size_t(tile * TILE + rr) * 256)[pr] = (c0 & 0xffffu) | (c1 << 16);
+        }
       }
     }
     tc::fence_before();
-    __syncthreads();  // TMEM / sA / stage reused by the next tile
+    __syncthreads();  // TMEM / sA / stage / red reused by the next tile
     tc::fence_after();
   }
   __syncthreads();
@@ -314,7 +381,7 @@ void launch_head(pcc_ctx c, const int8_t* F, uint32_t n, const DHead& L, const u
   }
   const uint32_t ntiles = (n + TILE - 1) / TILE;
   const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 2u));
-  kern<<<grid, TILE, SmemLayout::END, c->stream>>>(F, n, L.W1, L.b1, L.rq1, L.W2, L.b2, L.rql, lut, X, cf, cdf, a_dbg);
+  kern<<<grid, NT, SmemLayout::END, c->stream>>>(F, n, L.W1, L.b1, L.rq1, L.W2, L.b2, L.rql, lut, X, cf, cdf, a_dbg);
   launched(c);
 }
 
