@@ -172,8 +172,27 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     phase ^= 1u;
     tc::fence_after();
 
-    // ---- pass 1: Q8 logits (back into TMEM), local max / first argmax ----
-    int32_t lmax = INT32_MIN;
+    // ---- pass 1: max of z (the requant is monotone non-decreasing, m >= 0, so
+    //      max_i lq(z_i) = lq(max_i z_i)) ----
+    int32_t zmax = INT32_MIN;
+#pragma unroll 1
+    for (int ch = 0; ch < 4; ++ch) {
+      uint32_t v[16];
+      tmem_ld16(taddr + ch * 16, v);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int i = 64 * q + ch * 16 + k;
+        if (i < NCODE) zmax = max(zmax, int32_t(v[k]) + sb2[i]);
+      }
+    }
+    red[(q * TILE + r) * 2] = zmax;
+    __syncthreads();
+    const int32_t mu = lq8(max(max(red[r * 2], red[(TILE + r) * 2]), max(red[(2 * TILE + r) * 2], red[(3 * TILE + r) * 2])),
+                           rql);
+    // ---- pass 2: Q8 logit, e = LUT[delta >> 2] (0 beyond 16 nats), local sum and
+    //      local first index with delta == 0 (e stored back into TMEM) ----
+    uint32_t ssum = 0;
     int ist = 1 << 30;
 #pragma unroll 1
     for (int ch = 0; ch < 4; ++ch) {
@@ -183,36 +202,9 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const int i = 64 * q + ch * 16 + k;
-        const int32_t l = lq8(int32_t(v[k]) + sb2[i], rql);
-        v[k] = uint32_t(l);
-        if (i < NCODE && l > lmax) {
-          lmax = l;
-          ist = i;
-        }
-      }
-      tmem_st16(taddr + ch * 16, v);
-    }
-    red[(q * TILE + r) * 2] = lmax;
-    red[(q * TILE + r) * 2 + 1] = ist;
-    __syncthreads();
-    int32_t mu = red[r * 2];
-    for (int qq = 1; qq < 4; ++qq) mu = max(mu, red[(qq * TILE + r) * 2]);
-    int istar = 1 << 30;
-    for (int qq = 3; qq >= 0; --qq)
-      if (red[(qq * TILE + r) * 2] == mu) istar = red[(qq * TILE + r) * 2 + 1];
-    tmem_wait_st();
-    // ---- pass 2: e = LUT[delta >> 2] (0 beyond 16 nats), local sum ----
-    uint32_t ssum = 0;
-#pragma unroll 1
-    for (int ch = 0; ch < 4; ++ch) {
-      uint32_t v[16];
-      tmem_ld16(taddr + ch * 16, v);
-      tc::tmem_wait_ld();
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int i = 64 * q + ch * 16 + k;
-        const uint32_t dl = uint32_t(mu - int32_t(v[k]));
+        const uint32_t dl = uint32_t(mu - lq8(int32_t(v[k]) + sb2[i], rql));
         const uint32_t e = (i < NCODE && dl < 4096u) ? sLut[dl >> 2] : 0u;
+        if (i < NCODE && dl == 0u && ist > i) ist = i;
         v[k] = e;
         ssum += e;
       }
@@ -220,9 +212,12 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     }
     __syncthreads();  // everyone has read red (pass-1 values) before it is overwritten
     red[(q * TILE + r) * 2] = int32_t(ssum);
+    red[(q * TILE + r) * 2 + 1] = ist;
     __syncthreads();
     const uint32_t Ssum = uint32_t(red[r * 2]) + uint32_t(red[(TILE + r) * 2]) + uint32_t(red[(2 * TILE + r) * 2]) +
                           uint32_t(red[(3 * TILE + r) * 2]);
+    const int istar = min(min(red[r * 2 + 1], red[(TILE + r) * 2 + 1]),
+                          min(red[(2 * TILE + r) * 2 + 1], red[(3 * TILE + r) * 2 + 1]));
     tmem_wait_st();
     // ---- pass 3: p = 1 + floor(e * 65281 / S) (exact), leftover to the first argmax ----
     const uint64_t inv = ~0ull / uint64_t(Ssum);

@@ -4,6 +4,7 @@
 // One warp per segment; lane k owns symbols j = s*K + k.  Encoder runs steps in reverse
 // and places each renormalisation word by ballot so the stream is in decoder order.
 #include "pcc_internal.cuh"
+#include "tc.cuh"
 
 namespace pcc {
 
@@ -68,7 +69,8 @@ constexpr int DEC_STAGES = 4;
 __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs, int nseg, const uint8_t* __restrict__ bs,
                                                  const uint16_t* __restrict__ cdf, uint8_t* __restrict__ X,
                                                  uint32_t* __restrict__ err, int stage_rows) {
-  extern __shared__ __align__(16) uint16_t rows[];  // [DEC_STAGES][stage_rows][256]
+  extern __shared__ __align__(128) uint16_t rows[];  // [DEC_STAGES][stage_rows][256]
+  __shared__ __align__(8) uint64_t dec_mbar[DEC_STAGES];
   const int gw = blockIdx.x;
   const int lane = threadIdx.x;
   if (gw >= nseg) return;
@@ -110,23 +112,26 @@ __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs
   const uint32_t steps = (n + uint32_t(K) - 1u) / uint32_t(K);
   const uint16_t* base = cdf + size_t(sg.node) * 256;
   const unsigned lt = (1u << lane) - 1u;
+  // The K rows of a step are contiguous (nodes s*K .. s*K+K-1): one TMA bulk copy per
+  // step, issued by lane 0, completing on that stage's mbarrier.
+  if (lane == 0)
+    for (int st = 0; st < DEC_STAGES; ++st) tc::mbar_init(&dec_mbar[st], 1);
+  __syncwarp();
   auto prefetch = [&](uint32_t s) {
-    if (s < steps) {
-      uint16_t* buf = rows + size_t(s % DEC_STAGES) * stage_rows * 256;
-      for (int r = 0; r < K; ++r) {
-        const uint32_t j = s * uint32_t(K) + uint32_t(r);
-        if (j < n) cp_async16(buf + r * 256 + lane * 8, base + size_t(j) * 256 + lane * 8);
-      }
+    if (lane == 0 && s < steps) {
+      const uint32_t j0 = s * uint32_t(K);
+      const uint32_t nr = (n - j0) < uint32_t(K) ? (n - j0) : uint32_t(K);
+      uint64_t* mb = &dec_mbar[s % DEC_STAGES];
+      tc::mbar_expect_tx(mb, nr * 512u);
+      tc::bulk_g2s(rows + size_t(s % DEC_STAGES) * stage_rows * 256, base + size_t(j0) * 256, nr * 512u, mb);
     }
-    cp_commit();  // always commit (possibly empty) so group counting stays uniform
   };
 #pragma unroll
   for (int p = 0; p < DEC_STAGES - 1; ++p) prefetch(uint32_t(p));
   uint32_t used = 0;
   for (uint32_t s = 0; s < steps; ++s) {
     prefetch(s + DEC_STAGES - 1);
-    cp_wait<DEC_STAGES - 1>();
-    __syncwarp();
+    tc::mbar_wait(&dec_mbar[s % DEC_STAGES], (s / DEC_STAGES) & 1u);
     const uint32_t j = s * uint32_t(K) + uint32_t(lane);
     const bool act = lane < K && j < n;
     bool need = false;
@@ -166,7 +171,6 @@ __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs
     }
     __syncwarp();
   }
-  cp_wait<0>();
   if (used != W || (lane < K && x != (1u << 16))) bad = true;
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, EF_CORRUPT);
 }

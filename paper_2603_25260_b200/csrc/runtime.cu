@@ -145,7 +145,8 @@ struct Rd {
     t.mp = i32();
     t.mn = i32();
     t.r = i32();
-    if (t.r < 0 || t.r > 62) throw Error{PCC_ERR_INVALID_ARG};
+    // reading O5: m in [0, 2^31), r in [0, 62] (m >= 0 keeps every requant monotone)
+    if (t.r < 0 || t.r > 62 || t.mp < 0 || t.mn < 0) throw Error{PCC_ERR_INVALID_ARG};
     return t;
   }
 };
