@@ -91,9 +91,10 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
                                                    const int8_t* __restrict__ W2, const int32_t* __restrict__ b2, RQ rql,
                                                    const uint32_t* __restrict__ lut, const uint8_t* __restrict__ X,
                                                    uint32_t* __restrict__ cf, uint16_t* __restrict__ cdf,
-                                                   int8_t* __restrict__ a_dbg) {
+                                                   int8_t* __restrict__ a_dbg, int32_t zsat_lo, int32_t zsat_hi) {
   extern __shared__ __align__(1024) uint8_t sm[];
   using S = SmemLayout;
+  const int64_t lhalf = rql.r > 0 ? (int64_t(1) << (rql.r - 1)) : 0;
   uint8_t* sB = sm + S::B;
   uint8_t* sA = sm + S::A;
   uint32_t* sLut = reinterpret_cast<uint32_t*>(sm + S::LUT);
@@ -202,7 +203,12 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const int i = 64 * q + ch * 16 + k;
-        const uint32_t dl = uint32_t(mu - lq8(int32_t(v[k]) + sb2[i], rql));
+        const int32_t zz = int32_t(v[k]) + sb2[i];
+        // lq8(zz) without the 64-bit clamp: saturation decided in the z domain
+        const int32_t lv = zz > zsat_hi ? (1 << 24)
+                           : zz < zsat_lo ? -(1 << 24)
+                                          : int32_t((int64_t(zz) * rql.mp + lhalf) >> rql.r);
+        const uint32_t dl = uint32_t(mu - lv);
         const uint32_t e = (i < NCODE && dl < 4096u) ? sLut[dl >> 2] : 0u;
         if (i < NCODE && dl == 0u && ist > i) ist = i;
         v[k] = e;
@@ -220,7 +226,10 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
                           min(red[(2 * TILE + r) * 2 + 1], red[(3 * TILE + r) * 2 + 1]));
     tmem_wait_st();
     // ---- pass 3: p = 1 + floor(e * 65281 / S) (exact), leftover to the first argmax ----
-    const uint64_t inv = ~0ull / uint64_t(Ssum);
+    // q = floor(e * 65281 / S): estimate with the 32-bit reciprocal inv32 =
+    // floor(65281 * 2^32 / S) (< 2^24 since S >= LUT[0] = 2^24), q_est in {q - 1, q},
+    // then one exact 64-bit correction.
+    const uint32_t inv32 = uint32_t((65281ull << 32) / uint64_t(Ssum));
     uint32_t tot = 0;
     if constexpr (MODE == 0) {
       const int sym = valid ? int(X[row]) - 1 : 0;
@@ -233,9 +242,8 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const int i = 64 * q + ch * 16 + k;
-          const uint64_t num = uint64_t(v[k]) * 65281ull;
-          uint64_t qt = __umul64hi(num, inv);
-          if (num - qt * uint64_t(Ssum) >= uint64_t(Ssum)) ++qt;
+          uint32_t qt = __umulhi(v[k], inv32);
+          if (uint64_t(v[k]) * 65281ull - uint64_t(qt) * Ssum >= uint64_t(Ssum)) ++qt;
           const uint32_t p = (i < NCODE) ? uint32_t(1 + qt) : 0u;
           tot += p;
           cum += (i < sym) ? p : 0u;
@@ -274,9 +282,8 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
           uint32_t c2[2];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const uint64_t num = uint64_t(v[k + u]) * 65281ull;
-            uint64_t qt = __umul64hi(num, inv);
-            if (num - qt * uint64_t(Ssum) >= uint64_t(Ssum)) ++qt;
+            uint32_t qt = __umulhi(v[k + u], inv32);
+            if (uint64_t(v[k + u]) * 65281ull - uint64_t(qt) * Ssum >= uint64_t(Ssum)) ++qt;
             const uint32_t p = (i + u < NCODE) ? uint32_t(1 + qt) : 0u;
             c2[u] = run;  // quarter-local prefix (< 2^16)
             run += p;
@@ -376,7 +383,8 @@ void launch_head(pcc_ctx c, const int8_t* F, uint32_t n, const DHead& L, const u
   }
   const uint32_t ntiles = (n + TILE - 1) / TILE;
   const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 2u));
-  kern<<<grid, NT, SmemLayout::END, c->stream>>>(F, n, L.W1, L.b1, L.rq1, L.W2, L.b2, L.rql, lut, X, cf, cdf, a_dbg);
+  kern<<<grid, NT, SmemLayout::END, c->stream>>>(F, n, L.W1, L.b1, L.rq1, L.W2, L.b2, L.rql, lut, X, cf, cdf, a_dbg,
+                                                 L.zsat_lo, L.zsat_hi);
   launched(c);
 }
 

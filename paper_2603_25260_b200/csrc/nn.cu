@@ -202,53 +202,27 @@ __global__ void __launch_bounds__(128) k_up(const int8_t* __restrict__ S, const 
     const int x = Xp[p];
     int32_t v[C / 4];
     load_row<C / 4>(S + size_t(p) * C, v);
-    const int32_t* er = E + size_t(x - 1) * (8 * C) + c * C;
-    const int32_t* br = bias + c * C;
+    const int4* er4 = reinterpret_cast<const int4*>(E + size_t(x - 1) * (8 * C) + c * C);  // 16-B aligned rows
+    const int4* br4 = reinterpret_cast<const int4*>(bias + c * C);
+    int32_t eb[C];
+#pragma unroll
+    for (int k = 0; k < C / 4; ++k) {
+      const int4 e4 = er4[k], b4 = br4[k];
+      eb[4 * k] = e4.x + b4.x;
+      eb[4 * k + 1] = e4.y + b4.y;
+      eb[4 * k + 2] = e4.z + b4.z;
+      eb[4 * k + 3] = e4.w + b4.w;
+    }
     const int32_t* wr = Ws + c * CB;
 #pragma unroll
     for (int o = 0; o < C; ++o) {
-      int32_t a = br[o] + er[o];
+      int32_t a = eb[o];
 #pragma unroll
       for (int w = 0; w < C / 4; ++w) a = __dp4a(v[w], wr[o * (C / 4) + w], a);
       q[o] = rq8(a, rq);
     }
   }
   store_row<C>(out + size_t(j) * C, q);
-}
-
-// C = 32 variant: warp per kept child row, lane o = output channel o, so the parent
-// row is a broadcast load, the q_one*W_X row E[X][c] and the output row are coalesced,
-// and the transposed weights Wt[c][w][o] are read conflict-free.
-__global__ void __launch_bounds__(256) k_up_w32(const int8_t* __restrict__ S, const uint8_t* __restrict__ Xp,
-                                                const uint32_t* __restrict__ par, const uint64_t* __restrict__ key_c,
-                                                uint32_t nc, const int8_t* __restrict__ W, const int32_t* __restrict__ E,
-                                                const int32_t* __restrict__ bias, RQ rq, int8_t* __restrict__ out) {
-  constexpr int C = 32;
-  __shared__ int32_t Wt[8 * 8 * 32];
-  __shared__ int32_t bs[256];
-  for (int k = threadIdx.x; k < 8 * 8 * 32; k += blockDim.x) {
-    const int o = k & 31, w = (k >> 5) & 7, c = k >> 8;
-    Wt[k] = reinterpret_cast<const int32_t*>(W)[(c * C + o) * 8 + w];
-  }
-  for (int k = threadIdx.x; k < 256; k += blockDim.x) bs[k] = bias[k];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const uint32_t nw = gridDim.x * (blockDim.x / 32);
-  for (uint32_t j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); j <= nc; j += nw) {
-    int32_t q = 0;
-    if (j < nc) {
-      const uint32_t p = par[j];
-      const int c = int(key_c[j] & 7u);
-      const int x = Xp[p];
-      const int32_t sv = lane < 8 ? reinterpret_cast<const int32_t*>(S + size_t(p) * C)[lane] : 0;
-      int32_t acc = bs[c * C + lane] + E[size_t(x - 1) * (8 * C) + c * C + lane];
-      const int32_t* wt = Wt + c * 256 + lane;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) acc = __dp4a(__shfl_sync(0xffffffffu, sv, w), wt[w * 32], acc);
-      q = rq8(acc, rq);
-    }
-    out[size_t(j) * C + lane] = int8_t(q);
-  }
 }
 
 // ---- Predictor (Eq.7) + integer softmax to Q16 (Eq.15; readings Q20-Q22) -----------
@@ -462,11 +436,7 @@ void up_prune(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* par
   switch (C) {
     case 8: k_up<8><<<grid, 128, 0, c->stream>>>(S, Xp, par_c, key_c, nc, L.W, L.E, L.b, L.rq, out); break;
     case 16: k_up<16><<<grid, 128, 0, c->stream>>>(S, Xp, par_c, key_c, nc, L.W, L.E, L.b, L.rq, out); break;
-    case 32: {
-      const unsigned g = std::max(1u, std::min(cdiv(size_t(nc) + 1, 8), unsigned(c->sm_count) * 16u));
-      k_up_w32<<<g, 256, 0, c->stream>>>(S, Xp, par_c, key_c, nc, L.W, L.E, L.b, L.rq, out);
-      break;
-    }
+    case 32: k_up<32><<<grid, 128, 0, c->stream>>>(S, Xp, par_c, key_c, nc, L.W, L.E, L.b, L.rq, out); break;
     default: throw Error{PCC_ERR_INVALID_ARG};
   }
   launched(c);

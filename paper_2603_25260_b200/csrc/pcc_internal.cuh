@@ -45,6 +45,9 @@ struct DHead {       // Predictor: W1 [H][C], b1, rq1; W2 [256][H] (row 255 = 0)
   const int8_t* W2;
   const int32_t* b2;
   RQ rql;
+  // Saturation thresholds of the logit requant (exact, computed at load): z > zsat_hi
+  // gives +2^24, z < zsat_lo gives -2^24, otherwise the result fits in 32 bits.
+  int32_t zsat_lo, zsat_hi;
 };
 struct DShallow {
   DConv a, b;

@@ -170,6 +170,36 @@ uint64_t fnv1a(const uint8_t* p, size_t n) {
   return h;
 }
 
+// For l(z) = floor((z*m + h) / 2^r), h = 2^(r-1) (0 if r = 0), m >= 0, clamped to
+// [-T, T] with T = 2^24 (reading Q20): the int32 thresholds such that z > hi <=> l(z) >= T
+// and z < lo <=> l(z) <= -T.  Strictly between them |l| < T, so a kernel may compute
+// l from the low 32 bits of the 64-bit shift and skip the 64-bit clamp (exact).
+void logit_saturation(const RQ& q, int32_t& lo, int32_t& hi) {
+  const __int128 T = __int128(1) << 24;
+  const __int128 two_r = __int128(1) << q.r;
+  const __int128 h = q.r > 0 ? (__int128(1) << (q.r - 1)) : 0;
+  auto ceil_div = [](__int128 a, __int128 b) {  // b > 0
+    __int128 qq = a / b;
+    if (qq * b < a) ++qq;  // C++ division truncates toward zero
+    return qq;
+  };
+  __int128 zhi, zlo;  // zhi = min z with l >= T; zlo = max z with l <= -T
+  if (q.mp == 0) {
+    zhi = __int128(INT32_MAX) + 1;
+    zlo = __int128(INT32_MIN) - 1;
+  } else {
+    zhi = ceil_div(T * two_r - h, q.mp);
+    zlo = ceil_div((1 - T) * two_r - h, q.mp) - 1;
+  }
+  __int128 hx = zhi - 1, lx = zlo + 1;  // exclusive forms: z > hx, z < lx
+  if (hx > INT32_MAX) hx = INT32_MAX;
+  if (hx < INT32_MIN) hx = INT32_MIN;
+  if (lx < INT32_MIN) lx = INT32_MIN;
+  if (lx > INT32_MAX) lx = INT32_MAX;
+  hi = int32_t(hx);
+  lo = int32_t(lx);
+}
+
 // Pointers are staged as offsets and rebased after the single cudaMalloc.
 template <class T>
 T* off_ptr(size_t off) {
@@ -243,6 +273,7 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
       std::vector<int32_t> b2(256, 0);
       std::memcpy(b2.data(), r.take(size_t(4) * NCODE), size_t(4) * NCODE);
       hd.rql = r.rq();
+      logit_saturation(hd.rql, hd.zsat_lo, hd.zsat_hi);
       hd.W2 = off_ptr<const int8_t>(st.put(W2.data(), W2.size()));
       hd.b2 = off_ptr<const int32_t>(st.put(b2.data(), b2.size() * 4));
       return hd;
