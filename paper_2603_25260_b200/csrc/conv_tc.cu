@@ -1,0 +1,258 @@
+// conv_tc.cu — K3S1 integer sparse convolution on the 5th-generation tensor cores.
+//
+// sparse convolution "decomposed into multiple indexed linear
+// transforms"; Eq.13 (int8 x int8 -> int32, z_w = 0) and Eq.14 (fixed-point requant).
+// For a tile of 128 output rows and each kernel offset delta (27 of them, Eq.5/8/10 use
+// 3x3x3 kernels) the neighbour rows f[nbr[i][delta]] are GATHERED into a shared-memory
+// A tile (cp.async, 16-byte chunks, canonical K-major layout) and multiplied by W_delta
+// with one tcgen05.mma.kind::i8 (M = 128, N = C = 32, K = 32 per 32 input channels),
+// accumulating in TMEM (int32, 32 columns).  Absent neighbours index the all-zero row n.
+// Offsets with no neighbour in the whole tile are skipped.  A 3-stage ring of A tiles
+// overlaps the gather of offset k+2 with the MMA of offset k.  The XFP skip of conv_b
+// (a 1x1 projection P of [F_D | G_D], reading Q7) is one more MMA into the same
+// accumulator; the identity skip k_s * f is added in the epilogue.  Epilogue: tcgen05.ld
+// of the row's 32 accumulators, bias, skip, PReLU-requant, 32-byte store.
+// Bit-exact with the dp4a kernel and the oracle (int32 addition is associative, O6).
+#include "pcc_internal.cuh"
+#include "tc.cuh"
+
+namespace pcc {
+
+namespace {
+
+constexpr int CT = 128;      // rows per tile = threads per CTA
+constexpr int COUT = 32;
+constexpr int NSTAGE = 3;
+constexpr uint32_t IDESC32 = tc::idesc_i8(128, 32);
+
+__device__ __forceinline__ int32_t rq8(int32_t acc, RQ q) {
+  int64_t v = int64_t(acc) * int64_t(acc >= 0 ? q.mp : q.mn);
+  if (q.r > 0) v = (v + (int64_t(1) << (q.r - 1))) >> q.r;
+  return int32_t(v < -128 ? -128 : (v > 127 ? 127 : v));
+}
+
+__device__ __forceinline__ void cp16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// SLABS = input channels / 32 (1: C_in = 32; 2: the virtual concat [in0 | in1]).
+// SKIP: 0 none, 1 identity k_s * skip0, 2 projection P [32][64] of [skip0 | skip1].
+template <int SLABS, int SKIP>
+__global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0, const int8_t* __restrict__ in1,
+                                                 uint32_t n, const int32_t* __restrict__ nbr,
+                                                 const int8_t* __restrict__ W, const int32_t* __restrict__ bias, RQ rq,
+                                                 const int8_t* __restrict__ skip0, const int8_t* __restrict__ skip1,
+                                                 int32_t k_s, const int8_t* __restrict__ P, int8_t* __restrict__ out) {
+  constexpr int CIN = 32 * SLABS;
+  constexpr int BSLAB = COUT * 32;                  // 1 KB: one 32 x 32 B operand slab
+  constexpr int ASLAB = CT * 32;                    // 4 KB
+  constexpr int B_BYTES = 27 * SLABS * BSLAB;
+  constexpr int P_BYTES = SKIP == 2 ? 2 * BSLAB : 0;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* sB = sm;
+  uint8_t* sP = sm + B_BYTES;
+  uint8_t* sA = sm + B_BYTES + P_BYTES;                       // [NSTAGE][SLABS][ASLAB]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sA + NSTAGE * SLABS * ASLAB);  // [NSTAGE] + done
+  uint32_t* thold = reinterpret_cast<uint32_t*>(mbar + NSTAGE + 1);
+  uint32_t* omask = thold + 1;
+  int32_t* sbias = reinterpret_cast<int32_t*>(thold + 4);
+
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  // weights -> canonical K-major slabs: B[delta][s] element (o, k) = W[delta][o][32 s + k]
+  for (int k = t; k < 27 * COUT * (CIN / 4); k += CT) {
+    const int w = k % (CIN / 4), o = (k / (CIN / 4)) % COUT, dl = k / (COUT * (CIN / 4));
+    const int s = w / 8, kk = 4 * (w % 8);
+    *reinterpret_cast<uint32_t*>(sB + (dl * SLABS + s) * BSLAB + tc::kmaj_off(o, kk)) =
+        reinterpret_cast<const uint32_t*>(W)[k];
+  }
+  if (SKIP == 2)
+    for (int k = t; k < COUT * 16; k += CT) {
+      const int w = k % 16, o = k / 16, s = w / 8, kk = 4 * (w % 8);
+      *reinterpret_cast<uint32_t*>(sP + s * BSLAB + tc::kmaj_off(o, kk)) = reinterpret_cast<const uint32_t*>(P)[k];
+    }
+  for (int k = t; k < COUT; k += CT) sbias[k] = bias[k];
+  if (warp == 0) tc::tmem_alloc<32>(thold);
+  if (t == 0)
+    for (int i = 0; i <= NSTAGE; ++i) tc::mbar_init(&mbar[i], 1);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *thold;
+  uint32_t ph[NSTAGE + 1] = {0, 0, 0, 0};  // phase per barrier (uniform across threads)
+  const uint32_t ntiles = (n + 1 + CT - 1) / CT;  // rows 0..n (row n = the zero row)
+
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t i = tile * CT + t;
+    const bool valid = i < n;
+    // which offsets have at least one neighbour in this tile
+    if (t == 0) *omask = 0u;
+    __syncthreads();
+    uint32_t my = 0;
+    int32_t nb[27];
+#pragma unroll
+    for (int dl = 0; dl < 27; ++dl) {
+      nb[dl] = valid ? nbr[size_t(i) * 27 + dl] : int32_t(n);
+      if (nb[dl] != int32_t(n)) my |= 1u << dl;
+    }
+    my = __reduce_or_sync(0xffffffffu, my);
+    if (lane == 0) atomicOr(omask, my);
+    __syncthreads();
+    const uint32_t mask = *omask;
+    const int cnt = __popc(mask);
+    // gather for the k-th active offset into stage k % NSTAGE
+    auto gather = [&](int k) {
+      uint32_t m = mask;
+      for (int z = 0; z < k; ++z) m &= m - 1;
+      const int dl = __ffs(m) - 1;
+      int32_t j = int32_t(n);
+#pragma unroll
+      for (int d2 = 0; d2 < 27; ++d2)
+        if (d2 == dl) j = nb[d2];
+      uint8_t* a = sA + (k % NSTAGE) * SLABS * ASLAB;
+      cp16(a + tc::kmaj_off(t, 0), in0 + size_t(j) * 32);
+      cp16(a + tc::kmaj_off(t, 16), in0 + size_t(j) * 32 + 16);
+      if constexpr (SLABS == 2) {
+        cp16(a + ASLAB + tc::kmaj_off(t, 0), in1 + size_t(j) * 32);
+        cp16(a + ASLAB + tc::kmaj_off(t, 16), in1 + size_t(j) * 32 + 16);
+      }
+      return dl;
+    };
+    int dls[NSTAGE];
+    for (int k = 0; k < NSTAGE - 1; ++k) {
+      if (k < cnt) dls[k] = gather(k);
+      cp_commit();
+    }
+    for (int k = 0; k < cnt; ++k) {
+      const int kn = k + NSTAGE - 1;
+      if (kn < cnt) {
+        // stage kn % NSTAGE was last read by MMA kn - NSTAGE = k - 1
+        if (k >= 1) {
+          tc::mbar_wait(&mbar[kn % NSTAGE], ph[kn % NSTAGE]);
+          ph[kn % NSTAGE] ^= 1u;
+        }
+        dls[kn % NSTAGE] = gather(kn);
+      }
+      cp_commit();
+      cp_wait<NSTAGE - 1>();
+      tc::fence_async_smem();
+      __syncthreads();
+      if (t == 0) {
+        tc::fence_after();
+        const int dl = dls[k % NSTAGE];
+        const uint8_t* a = sA + (k % NSTAGE) * SLABS * ASLAB;
+#pragma unroll
+        for (int s = 0; s < SLABS; ++s)
+          tc::mma_i8(tmem, tc::sdesc(tc::smem_u32(a + s * ASLAB)), tc::sdesc(tc::smem_u32(sB + (dl * SLABS + s) * BSLAB)),
+                     IDESC32, (k > 0 || s > 0) ? 1u : 0u);
+        tc::commit(&mbar[k % NSTAGE]);
+      }
+    }
+    // consume the commits of the last min(cnt, NSTAGE-1) stages that were not waited on
+    for (int k = (cnt > NSTAGE - 1 ? cnt - (NSTAGE - 1) : 0); k < cnt; ++k) {
+      tc::mbar_wait(&mbar[k % NSTAGE], ph[k % NSTAGE]);
+      ph[k % NSTAGE] ^= 1u;
+    }
+    bool any = cnt > 0;
+    if constexpr (SKIP == 2) {  // 1x1 projection of the concat, own row
+      uint8_t* a = sA;  // all stages are free now
+      const uint32_t ii = valid ? i : n;
+      cp16(a + tc::kmaj_off(t, 0), skip0 + size_t(ii) * 32);
+      cp16(a + tc::kmaj_off(t, 16), skip0 + size_t(ii) * 32 + 16);
+      cp16(a + ASLAB + tc::kmaj_off(t, 0), skip1 + size_t(ii) * 32);
+      cp16(a + ASLAB + tc::kmaj_off(t, 16), skip1 + size_t(ii) * 32 + 16);
+      cp_commit();
+      cp_wait<0>();
+      tc::fence_async_smem();
+      __syncthreads();
+      if (t == 0) {
+        tc::fence_after();
+        tc::mma_i8(tmem, tc::sdesc(tc::smem_u32(a)), tc::sdesc(tc::smem_u32(sP)), IDESC32, any ? 1u : 0u);
+        tc::mma_i8(tmem, tc::sdesc(tc::smem_u32(a + ASLAB)), tc::sdesc(tc::smem_u32(sP + BSLAB)), IDESC32, 1u);
+      }
+      any = true;
+    }
+    if (t == 0) tc::commit(&mbar[NSTAGE]);
+    tc::mbar_wait(&mbar[NSTAGE], ph[NSTAGE]);
+    ph[NSTAGE] ^= 1u;
+    tc::fence_after();
+    // ---- epilogue ----
+    uint32_t v[32];
+    tc::tmem_ld32(tmem + (uint32_t(warp * 32) << 16), v);
+    tc::tmem_wait_ld();
+    if (i <= n) {
+      int32_t acc[32];
+#pragma unroll
+      for (int o = 0; o < 32; ++o) acc[o] = any ? int32_t(v[o]) : 0;
+      uint32_t w[8];
+      if (i < n) {
+        if constexpr (SKIP == 1) {
+          const int4* s4 = reinterpret_cast<const int4*>(skip0 + size_t(i) * 32);
+          const int4 a0 = s4[0], a1 = s4[1];
+          const uint32_t sw[8] = {uint32_t(a0.x), uint32_t(a0.y), uint32_t(a0.z), uint32_t(a0.w),
+                                  uint32_t(a1.x), uint32_t(a1.y), uint32_t(a1.z), uint32_t(a1.w)};
+#pragma unroll
+          for (int o = 0; o < 32; ++o) acc[o] += k_s * int32_t(int8_t(sw[o >> 2] >> (8 * (o & 3))));
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          uint32_t pk = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) pk |= (uint32_t(rq8(acc[4 * k + u] + sbias[4 * k + u], rq)) & 0xffu) << (8 * u);
+          w[k] = pk;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = 0u;  // the zero row
+      }
+      uint4* o4 = reinterpret_cast<uint4*>(out + size_t(i) * 32);
+      o4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      o4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+    tc::fence_before();
+    __syncthreads();  // TMEM and A stages reused by the next tile
+    tc::fence_after();
+  }
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<32>(tmem);
+}
+
+template <int SLABS, int SKIP>
+void launch(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,
+            const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out) {
+  constexpr int smem = 27 * SLABS * 1024 + (SKIP == 2 ? 2048 : 0) + NSTAGE * SLABS * 4096 + 64 + 128;
+  auto kern = k_conv3_tc<SLABS, SKIP>;
+  static bool attr = false;
+  if (!attr) {
+    PCC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  // the zero row n belongs to tile n / CT: cover rows 0..n
+  const uint32_t ntiles = (n + 1 + CT - 1) / CT;
+  const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 3u));
+  Prof p(c, "conv", size_t(n) * (32 * SLABS + 32 + 27 * 4 + (SKIP ? (SKIP == 2 ? 64 : 32) : 0)));
+  kern<<<grid, CT, smem, c->stream>>>(in0, in1, n, nbr, L.W, L.b, L.rq, s0, s1, k_s, P, out);
+  launched(c);
+}
+
+}  // namespace
+
+// C = 32 only (the tcgen05 K slab is 32 channels); other widths use the dp4a kernel.
+void conv3_tc(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,
+              int skip_mode, const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out) {
+  if (in1) {
+    if (skip_mode != 0) throw Error{PCC_ERR_INVALID_ARG};
+    launch<2, 0>(c, in0, in1, n, nbr, L, s0, s1, k_s, P, out);
+  } else if (skip_mode == 0) {
+    launch<1, 0>(c, in0, nullptr, n, nbr, L, s0, s1, k_s, P, out);
+  } else if (skip_mode == 1) {
+    launch<1, 1>(c, in0, nullptr, n, nbr, L, s0, s1, k_s, P, out);
+  } else {
+    launch<1, 2>(c, in0, nullptr, n, nbr, L, s0, s1, k_s, P, out);
+  }
+}
+
+}  // namespace pcc

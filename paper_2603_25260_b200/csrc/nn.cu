@@ -408,6 +408,16 @@ void embed(pcc_ctx c, const int8_t* E, const uint8_t* X, uint32_t n, int C, int8
 
 void conv3(pcc_ctx c, const int8_t* in0, const int8_t* in1, int C, uint32_t n, const int32_t* nbr, const DConv& L,
            int skip_mode, const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out) {
+  // C = 32: gather -> tcgen05 kind::i8 per kernel offset (conv_tc.cu); PCC_CONV=simt
+  // keeps the dp4a kernel (A/B baseline, bit-exact with it).
+  static const bool simt = [] {
+    const char* e = getenv("PCC_CONV");
+    return e && std::string(e) == "simt";
+  }();
+  if (C == 32 && !simt) {
+    conv3_tc(c, in0, in1, n, nbr, L, skip_mode, s0, s1, k_s, P, out);
+    return;
+  }
   switch (C) {
     case 8: conv3_c<8>(c, in0, in1, n, nbr, L, skip_mode, s0, s1, k_s, P, out); break;
     case 16: conv3_c<16>(c, in0, in1, n, nbr, L, skip_mode, s0, s1, k_s, P, out); break;

@@ -51,17 +51,9 @@ __device__ __forceinline__ uint32_t ld_u32(const uint8_t* p) {
   return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
-  const uint32_t s = uint32_t(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 // Decoder: one warp per segment (block = 1 warp).  The CDF rows of the K nodes of a step
 // do not depend on the rANS state, so they are prefetched DEC_STAGES steps ahead into
-// shared memory with cp.async; the renormalisation words are consumed in stream order
+// shared memory with TMA bulk copies; the renormalisation words are consumed in stream order
 // and are held in a 96-word register window (three words per lane) refilled 64 words
 // ahead, so no step waits on a dependent global load.
 constexpr int DEC_STAGES = 4;
