@@ -151,8 +151,9 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
         tc::commit(&mbar[k % NSTAGE]);
       }
     }
-    // consume the commits of the last min(cnt, NSTAGE-1) stages that were not waited on
-    for (int k = (cnt > NSTAGE - 1 ? cnt - (NSTAGE - 1) : 0); k < cnt; ++k) {
+    // the loop waited on MMAs 0..cnt-NSTAGE-1 (before reusing their stage); consume the
+    // commits of the last min(cnt, NSTAGE) so every barrier phase is waited exactly once
+    for (int k = (cnt > NSTAGE ? cnt - NSTAGE : 0); k < cnt; ++k) {
       tc::mbar_wait(&mbar[k % NSTAGE], ph[k % NSTAGE]);
       ph[k % NSTAGE] ^= 1u;
     }
