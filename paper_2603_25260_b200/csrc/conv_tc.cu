@@ -7,8 +7,9 @@
 // A tile (cp.async, 16-byte chunks, canonical K-major layout) and multiplied by W_delta
 // with one tcgen05.mma.kind::i8 (M = 128, N = C = 32, K = 32 per 32 input channels),
 // accumulating in TMEM (int32, 32 columns).  Absent neighbours index the all-zero row n.
-// Offsets with no neighbour in the whole tile are skipped.  A 3-stage ring of A tiles
-// overlaps the gather of offset k+2 with the MMA of offset k.  The XFP skip of conv_b
+// Offsets with no neighbour in the whole tile are skipped.  Active offsets are gathered
+// in groups (one barrier per group) into two alternating A buffers, so the gather of
+// group g+1 overlaps the MMAs of group g.  The XFP skip of conv_b
 // (a 1x1 projection P of [F_D | G_D], reading Q7) is one more MMA into the same
 // accumulator; the identity skip k_s * f is added in the epilogue.  Epilogue: tcgen05.ld
 // of the row's 32 accumulators, bias, skip, PReLU-requant, 32-byte store.
@@ -22,7 +23,9 @@ namespace {
 
 constexpr int CT = 128;      // rows per tile = threads per CTA
 constexpr int COUT = 32;
-constexpr int NSTAGE = 3;
+constexpr int NSTAGE = 3;  // barrier slots: 0, 1 = A buffers, NSTAGE = tile done
+// kernel offsets gathered per barrier (2 A buffers of GROUP x SLABS x 4 KB; 2 CTAs/SM)
+__host__ __device__ constexpr int group_of(int slabs) { return slabs == 1 ? 7 : 3; }
 constexpr uint32_t IDESC32 = tc::idesc_i8(128, 32);
 
 __device__ __forceinline__ int32_t rq8(int32_t acc, RQ q) {
@@ -54,8 +57,9 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* sB = sm;
   uint8_t* sP = sm + B_BYTES;
-  uint8_t* sA = sm + B_BYTES + P_BYTES;                       // [NSTAGE][SLABS][ASLAB]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sA + NSTAGE * SLABS * ASLAB);  // [NSTAGE] + done
+  constexpr int GROUP = group_of(SLABS);
+  uint8_t* sA = sm + B_BYTES + P_BYTES;                       // [2][GROUP][SLABS][ASLAB]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sA + 2 * GROUP * SLABS * ASLAB);  // [0,1] buffers, [NSTAGE] done
   uint32_t* thold = reinterpret_cast<uint32_t*>(mbar + NSTAGE + 1);
   uint32_t* omask = thold + 1;
   int32_t* sbias = reinterpret_cast<int32_t*>(thold + 4);
@@ -103,59 +107,61 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
     __syncthreads();
     const uint32_t mask = *omask;
     const int cnt = __popc(mask);
-    // gather for the k-th active offset into stage k % NSTAGE
-    auto gather = [&](int k) {
+    // Active offsets are processed in groups of GROUP: every thread issues the gathers of
+    // the whole group at once (GROUP x SLABS x 2 cp.async in flight), then ONE barrier,
+    // then the group's MMAs back to back and one commit.  Groups alternate between two
+    // A buffers, so the gather of group g+1 overlaps the MMAs of group g.
+    int done = 0;  // active offsets consumed
+    for (int g = 0; done < cnt; ++g) {
+      const int b = g & 1;
+      if (g >= 2) {  // buffer b was read by the MMAs of group g-2
+        tc::mbar_wait(&mbar[b], ph[b]);
+        ph[b] ^= 1u;
+      }
+      uint8_t* abuf = sA + b * GROUP * SLABS * ASLAB;
+      int dls[GROUP];
+      int ng = 0;
       uint32_t m = mask;
-      for (int z = 0; z < k; ++z) m &= m - 1;
-      const int dl = __ffs(m) - 1;
-      int32_t j = int32_t(n);
+      for (int z = 0; z < done; ++z) m &= m - 1;
+      for (; ng < GROUP && m; ++ng) {
+        const int dl = __ffs(m) - 1;
+        m &= m - 1;
+        dls[ng] = dl;
+        int32_t j = int32_t(n);
 #pragma unroll
-      for (int d2 = 0; d2 < 27; ++d2)
-        if (d2 == dl) j = nb[d2];
-      uint8_t* a = sA + (k % NSTAGE) * SLABS * ASLAB;
-      cp16(a + tc::kmaj_off(t, 0), in0 + size_t(j) * 32);
-      cp16(a + tc::kmaj_off(t, 16), in0 + size_t(j) * 32 + 16);
-      if constexpr (SLABS == 2) {
-        cp16(a + ASLAB + tc::kmaj_off(t, 0), in1 + size_t(j) * 32);
-        cp16(a + ASLAB + tc::kmaj_off(t, 16), in1 + size_t(j) * 32 + 16);
-      }
-      return dl;
-    };
-    int dls[NSTAGE];
-    for (int k = 0; k < NSTAGE - 1; ++k) {
-      if (k < cnt) dls[k] = gather(k);
-      cp_commit();
-    }
-    for (int k = 0; k < cnt; ++k) {
-      const int kn = k + NSTAGE - 1;
-      if (kn < cnt) {
-        // stage kn % NSTAGE was last read by MMA kn - NSTAGE = k - 1
-        if (k >= 1) {
-          tc::mbar_wait(&mbar[kn % NSTAGE], ph[kn % NSTAGE]);
-          ph[kn % NSTAGE] ^= 1u;
+        for (int d2 = 0; d2 < 27; ++d2)
+          if (d2 == dl) j = nb[d2];
+        uint8_t* a = abuf + ng * SLABS * ASLAB;
+        cp16(a + tc::kmaj_off(t, 0), in0 + size_t(j) * 32);
+        cp16(a + tc::kmaj_off(t, 16), in0 + size_t(j) * 32 + 16);
+        if constexpr (SLABS == 2) {
+          cp16(a + ASLAB + tc::kmaj_off(t, 0), in1 + size_t(j) * 32);
+          cp16(a + ASLAB + tc::kmaj_off(t, 16), in1 + size_t(j) * 32 + 16);
         }
-        dls[kn % NSTAGE] = gather(kn);
       }
       cp_commit();
-      cp_wait<NSTAGE - 1>();
+      cp_wait<0>();
       tc::fence_async_smem();
       __syncthreads();
       if (t == 0) {
         tc::fence_after();
-        const int dl = dls[k % NSTAGE];
-        const uint8_t* a = sA + (k % NSTAGE) * SLABS * ASLAB;
+        for (int k = 0; k < ng; ++k) {
+          const uint8_t* a = abuf + k * SLABS * ASLAB;
 #pragma unroll
-        for (int s = 0; s < SLABS; ++s)
-          tc::mma_i8(tmem, tc::sdesc(tc::smem_u32(a + s * ASLAB)), tc::sdesc(tc::smem_u32(sB + (dl * SLABS + s) * BSLAB)),
-                     IDESC32, (k > 0 || s > 0) ? 1u : 0u);
-        tc::commit(&mbar[k % NSTAGE]);
+          for (int s = 0; s < SLABS; ++s)
+            tc::mma_i8(tmem, tc::sdesc(tc::smem_u32(a + s * ASLAB)),
+                       tc::sdesc(tc::smem_u32(sB + (dls[k] * SLABS + s) * BSLAB)), IDESC32,
+                       (done + k > 0 || s > 0) ? 1u : 0u);
+        }
+        tc::commit(&mbar[b]);
       }
-    }
-    // the loop waited on MMAs 0..cnt-NSTAGE-1 (before reusing their stage); consume the
-    // commits of the last min(cnt, NSTAGE) so every barrier phase is waited exactly once
-    for (int k = (cnt > NSTAGE ? cnt - NSTAGE : 0); k < cnt; ++k) {
-      tc::mbar_wait(&mbar[k % NSTAGE], ph[k % NSTAGE]);
-      ph[k % NSTAGE] ^= 1u;
+      done += ng;
+      if (done >= cnt) {  // drain: consume the commits of the last one or two groups
+        for (int gg = (g >= 1 ? g - 1 : 0); gg <= g; ++gg) {
+          tc::mbar_wait(&mbar[gg & 1], ph[gg & 1]);
+          ph[gg & 1] ^= 1u;
+        }
+      }
     }
     bool any = cnt > 0;
     if constexpr (SKIP == 2) {  // 1x1 projection of the concat, own row
@@ -224,7 +230,7 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
 template <int SLABS, int SKIP>
 void launch(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,
             const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out) {
-  constexpr int smem = 27 * SLABS * 1024 + (SKIP == 2 ? 2048 : 0) + NSTAGE * SLABS * 4096 + 64 + 128;
+  constexpr int smem = 27 * SLABS * 1024 + (SKIP == 2 ? 2048 : 0) + 2 * group_of(SLABS) * SLABS * 4096 + 64 + 128;
   auto kern = k_conv3_tc<SLABS, SKIP>;
   static bool attr = false;
   if (!attr) {
