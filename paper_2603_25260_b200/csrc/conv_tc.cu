@@ -66,16 +66,31 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   // weights -> canonical K-major slabs: B[delta][s] element (o, k) = W[delta][o][32 s + k]
-  for (int k = t; k < 27 * COUT * (CIN / 4); k += CT) {
-    const int w = k % (CIN / 4), o = (k / (CIN / 4)) % COUT, dl = k / (COUT * (CIN / 4));
-    const int s = w / 8, kk = 4 * (w % 8);
-    *reinterpret_cast<uint32_t*>(sB + (dl * SLABS + s) * BSLAB + tc::kmaj_off(o, kk)) =
-        reinterpret_cast<const uint32_t*>(W)[k];
+  // 16-byte chunks (one K half of one output row); all loads of a batch are issued
+  // before any store so the L2 latency is paid once per batch, not per chunk
+  {
+    constexpr int NCH = 27 * COUT * (CIN / 16);  // 16-byte chunks of W
+    constexpr int PER = (NCH + CT - 1) / CT;
+    uint4 buf[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int k = t + u * CT;
+      if (k < NCH) buf[u] = reinterpret_cast<const uint4*>(W)[k];
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int k = t + u * CT;  // chunk k = (dl, o, h): h = 16-byte piece of the CIN-byte row
+      if (k < NCH) {
+        const int h = k % (CIN / 16), o = (k / (CIN / 16)) % COUT, dl = k / (COUT * (CIN / 16));
+        *reinterpret_cast<uint4*>(sB + (dl * SLABS + h / 2) * BSLAB + tc::kmaj_off(o, 16 * (h % 2))) = buf[u];
+      }
+    }
   }
   if (SKIP == 2)
-    for (int k = t; k < COUT * 16; k += CT) {
-      const int w = k % 16, o = k / 16, s = w / 8, kk = 4 * (w % 8);
-      *reinterpret_cast<uint32_t*>(sP + s * BSLAB + tc::kmaj_off(o, kk)) = reinterpret_cast<const uint32_t*>(P)[k];
+    for (int k = t; k < COUT * 4; k += CT) {  // P [32][64]: 4 chunks per row
+      const int h = k % 4, o = k / 4;
+      *reinterpret_cast<uint4*>(sP + (h / 2) * BSLAB + tc::kmaj_off(o, 16 * (h % 2))) =
+          reinterpret_cast<const uint4*>(P)[k];
     }
   for (int k = t; k < COUT; k += CT) sbias[k] = bias[k];
   if (warp == 0) tc::tmem_alloc<32>(thold);
