@@ -23,6 +23,23 @@ namespace {
 
 constexpr int CT = 128;      // rows per tile = threads per CTA
 constexpr int COUT = 32;
+#ifdef PCC_TRACE
+// development-only phase timer (tools/micro/trace_conv.py): cycles per phase, CTA thread 0
+__device__ unsigned long long g_conv_trace[8];
+#define CONV_TRACE(slot, t0)                                                     \
+  do {                                                                           \
+    if (threadIdx.x == 0) {                                                      \
+      const long long t1_ = clock64();                                           \
+      atomicAdd(&g_conv_trace[slot], (unsigned long long)(t1_ - (t0)));         \
+      (t0) = t1_;                                                                \
+    }                                                                            \
+  } while (0)
+#else
+#define CONV_TRACE(slot, t0) \
+  do {                       \
+  } while (0)
+#endif
+
 constexpr int NSTAGE = 3;  // barrier slots: 0, 1 = A buffers, NSTAGE = tile done
 // kernel offsets gathered per barrier (2 A buffers of GROUP x SLABS x 4 KB; 2 CTAs/SM)
 __host__ __device__ constexpr int group_of(int slabs) { return slabs == 1 ? 7 : 3; }
@@ -65,6 +82,7 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
   int32_t* sbias = reinterpret_cast<int32_t*>(thold + 4);
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  long long tr0 = clock64();
   // weights -> canonical K-major slabs: B[delta][s] element (o, k) = W[delta][o][32 s + k]
   // 16-byte chunks (one K half of one output row); all loads of a batch are issued
   // before any store so the L2 latency is paid once per batch, not per chunk
@@ -101,6 +119,7 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *thold;
+  CONV_TRACE(0, tr0);
   uint32_t ph[NSTAGE + 1] = {0, 0, 0, 0};  // phase per barrier (uniform across threads)
   const uint32_t ntiles = (n + 1 + CT - 1) / CT;  // rows 0..n (row n = the zero row)
 
@@ -121,6 +140,7 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
     if (lane == 0) atomicOr(omask, my);
     __syncthreads();
     const uint32_t mask = *omask;
+    CONV_TRACE(1, tr0);
     const int cnt = __popc(mask);
     // Active offsets are processed in groups of GROUP: every thread issues the gathers of
     // the whole group at once (GROUP x SLABS x 2 cp.async in flight), then ONE barrier,
@@ -147,11 +167,20 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
         for (int d2 = 0; d2 < 27; ++d2)
           if (d2 == dl) j = nb[d2];
         uint8_t* a = abuf + ng * SLABS * ASLAB;
-        cp16(a + tc::kmaj_off(t, 0), in0 + size_t(j) * 32);
-        cp16(a + tc::kmaj_off(t, 16), in0 + size_t(j) * 32 + 16);
-        if constexpr (SLABS == 2) {
-          cp16(a + ASLAB + tc::kmaj_off(t, 0), in1 + size_t(j) * 32);
-          cp16(a + ASLAB + tc::kmaj_off(t, 16), in1 + size_t(j) * 32 + 16);
+        if (j != int32_t(n)) {
+          cp16(a + tc::kmaj_off(t, 0), in0 + size_t(j) * 32);
+          cp16(a + tc::kmaj_off(t, 16), in0 + size_t(j) * 32 + 16);
+          if constexpr (SLABS == 2) {
+            cp16(a + ASLAB + tc::kmaj_off(t, 0), in1 + size_t(j) * 32);
+            cp16(a + ASLAB + tc::kmaj_off(t, 16), in1 + size_t(j) * 32 + 16);
+          }
+        } else {  // absent neighbour: zeros written directly (no L2 hot spot on the zero row)
+          const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+          for (int s = 0; s < SLABS; ++s) {
+            *reinterpret_cast<uint4*>(a + s * ASLAB + tc::kmaj_off(t, 0)) = z;
+            *reinterpret_cast<uint4*>(a + s * ASLAB + tc::kmaj_off(t, 16)) = z;
+          }
         }
       }
       cp_commit();
@@ -178,6 +207,7 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
         }
       }
     }
+    CONV_TRACE(2, tr0);
     bool any = cnt > 0;
     if constexpr (SKIP == 2) {  // 1x1 projection of the concat, own row
       uint8_t* a = sA;  // all stages are free now
@@ -201,6 +231,7 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
     tc::mbar_wait(&mbar[NSTAGE], ph[NSTAGE]);
     ph[NSTAGE] ^= 1u;
     tc::fence_after();
+    CONV_TRACE(3, tr0);
     // ---- epilogue ----
     uint32_t v[32];
     tc::tmem_ld32(tmem + (uint32_t(warp * 32) << 16), v);
@@ -234,6 +265,7 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
       o4[0] = make_uint4(w[0], w[1], w[2], w[3]);
       o4[1] = make_uint4(w[4], w[5], w[6], w[7]);
     }
+    CONV_TRACE(4, tr0);
     tc::fence_before();
     __syncthreads();  // TMEM and A stages reused by the next tile
     tc::fence_after();
@@ -278,3 +310,14 @@ void conv3_tc(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const
 }
 
 }  // namespace pcc
+
+#ifdef PCC_TRACE
+extern "C" int pcc_trace_conv(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, pcc::g_conv_trace, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(pcc::g_conv_trace, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -16,7 +16,7 @@ import os
 from typing import Optional, Sequence, Tuple
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpcc.so")
+LIB_PATH = os.environ.get("PCC_LIB") or os.path.join(HERE, "libpcc.so")  # PCC_LIB: dev builds only
 
 STATUS = ["OK", "INVALID_ARG", "EMPTY", "RANGE", "UNSUPPORTED_DEPTH", "CAPACITY", "BAD_MAGIC", "VERSION",
           "MODEL_MISMATCH", "TRUNCATED", "CORRUPT", "CUDA", "OOM"]
