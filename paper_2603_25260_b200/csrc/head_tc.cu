@@ -185,6 +185,8 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     //      local first index with delta == 0 (e stored back into TMEM) ----
     uint32_t ssum = 0;
     int ist = 1 << 30;
+    const int64_t lm = rql.mp;
+    const int lr = rql.r;
 #pragma unroll 1
     for (int ch = 0; ch < 4; ++ch) {
       uint32_t v[16];
@@ -194,16 +196,20 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       for (int k = 0; k < 16; ++k) {
         const int i = 64 * q + ch * 16 + k;
         const int32_t zz = int32_t(v[k]) + sb2[i];
-        // lq8(zz) without the 64-bit clamp: saturation decided in the z domain
-        const int32_t lv = zz > zsat_hi ? (1 << 24)
-                           : zz < zsat_lo ? -(1 << 24)
-                                          : int32_t((int64_t(zz) * rql.mp + lhalf) >> rql.r);
+        // lq8(zz) without the 64-bit clamp: saturation is decided in the z domain and
+        // selected (branch-free) over the low word of the 64-bit shift
+        int32_t lv = int32_t((int64_t(zz) * lm + lhalf) >> lr);
+        lv = zz > zsat_hi ? (1 << 24) : lv;
+        lv = zz < zsat_lo ? -(1 << 24) : lv;
         const uint32_t dl = uint32_t(mu - lv);
-        const uint32_t e = (i < NCODE && dl < 4096u) ? sLut[dl >> 2] : 0u;
-        if (i < NCODE && dl == 0u && ist > i) ist = i;
+        const uint32_t e0 = sLut[min(dl, 4095u) >> 2];  // unconditional load: no branch
+        const uint32_t e = dl < 4096u ? e0 : 0u;
+        if (dl == 0u) ist = min(ist, i);  // i increases: the first index wins
         v[k] = e;
-        ssum += e;
       }
+      if (q == 3 && ch == 3) v[15] = 0u;  // column 255 is padding, not a symbol
+#pragma unroll
+      for (int k = 0; k < 16; ++k) ssum += v[k];
       tmem_st16(taddr + ch * 16, v);
     }
     __syncthreads();  // everyone has read red (pass-1 values) before it is overwritten
@@ -220,6 +226,26 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     // floor(65281 * 2^32 / S) (< 2^24 since S >= LUT[0] = 2^24), q_est in {q - 1, q},
     // then one exact 64-bit correction.
     const uint32_t inv32 = uint32_t((65281ull << 32) / uint64_t(Ssum));
+    // S <= 2^31: the remainder r = e*65281 - q_est*S lies in [0, 2S) subset [0, 2^32), so
+    // the correction is exact in 32-bit wrap-around arithmetic; otherwise use 64 bits.
+    const bool s32 = Ssum <= 0x80000000u;
+    // p = 1 + q for the 16 exponentials of a chunk (the s32 choice is per row, hoisted
+    // out of the element loop so only one variant is issued)
+    auto pchunk = [&](uint32_t (&v)[16]) {
+      if (s32) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const uint32_t qt = __umulhi(v[k], inv32);
+          v[k] = 1u + qt + ((v[k] * 65281u - qt * Ssum) >= Ssum ? 1u : 0u);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const uint32_t qt = __umulhi(v[k], inv32);
+          v[k] = 1u + qt + ((uint64_t(v[k]) * 65281ull - uint64_t(qt) * Ssum) >= uint64_t(Ssum) ? 1u : 0u);
+        }
+      }
+    };
     uint32_t tot = 0;
     if constexpr (MODE == 0) {
       const int sym = valid ? int(X[row]) - 1 : 0;
@@ -229,17 +255,16 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         uint32_t v[16];
         tmem_ld16(taddr + ch * 16, v);
         tc::tmem_wait_ld();
+        pchunk(v);
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const int i = 64 * q + ch * 16 + k;
-          uint32_t qt = __umulhi(v[k], inv32);
-          if (uint64_t(v[k]) * 65281ull - uint64_t(qt) * Ssum >= uint64_t(Ssum)) ++qt;
-          const uint32_t p = (i < NCODE) ? uint32_t(1 + qt) : 0u;
-          tot += p;
-          cum += (i < sym) ? p : 0u;
-          fq = (i == sym) ? p : fq;
+          tot += v[k];
+          cum += (i < sym) ? v[k] : 0u;
+          fq = (i == sym) ? v[k] : fq;
         }
       }
+      if (q == 3) tot -= 1u;  // the padding column 255 (e = 0 -> p = 1) is not a symbol
       __syncthreads();  // Ssum reads done
       red[(q * TILE + r) * 2] = int32_t(tot);
       red[(q * TILE + r) * 2 + 1] = int32_t(cum | (fq << 16));  // cum < 2^16 per quarter? use rowi
@@ -266,21 +291,20 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         uint32_t v[16];
         tmem_ld16(taddr + ch * 16, v);
         tc::tmem_wait_ld();
+        pchunk(v);
 #pragma unroll
         for (int k = 0; k < 16; k += 2) {
           const int i = 64 * q + ch * 16 + k;
           uint32_t c2[2];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            uint32_t qt = __umulhi(v[k + u], inv32);
-            if (uint64_t(v[k + u]) * 65281ull - uint64_t(qt) * Ssum >= uint64_t(Ssum)) ++qt;
-            const uint32_t p = (i + u < NCODE) ? uint32_t(1 + qt) : 0u;
             c2[u] = run;  // quarter-local prefix (< 2^16)
-            run += p;
+            run += v[k + u];
           }
           *reinterpret_cast<uint32_t*>(srow + i) = (c2[0] & 0xffffu) | (c2[1] << 16);
         }
       }
+      if (q == 3) run -= 1u;  // padding column 255
       __syncthreads();  // Ssum reads done
       red[(q * TILE + r) * 2] = int32_t(run);
       __syncthreads();
