@@ -190,6 +190,11 @@ void head_cdf_tc(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHe
                  const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg);
 void gemm_i8_test(pcc_ctx c, const int8_t* dA, const int8_t* dB, int N, int32_t* dD);
 
+// ---- up_tc.cu (parents x W_S on tcgen05, pruned epilogue; C = 32) ----
+// S: parent rows (np), Xp / cs_p: parent codes / child starts, nc: child rows (out has nc+1)
+void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* cs_p, uint32_t np, uint32_t nc,
+                 const DUp& L, int8_t* out);
+
 // ---- conv_tc.cu (gather -> tcgen05 kind::i8 per kernel offset; C = 32) ----
 void conv3_tc(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,
               int skip_mode, const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out);

@@ -382,6 +382,19 @@ struct Net {
 
   void dbgF(const std::string& name, const int8_t* p, uint32_t n, int width) { dbg_copy(c, name, p, size_t(n) * width); }
 
+  // Upsampling + Pruning from depth k to k+1 (Eq.6/9/11): tcgen05 kernel for C = 32
+  // (PCC_UP=simt keeps the dp4a kernel, the bit-exact A/B baseline).
+  void up(int k, const int8_t* S, const DUp& L, int8_t* dst) {
+    static const bool simt = [] {
+      const char* e = getenv("PCC_UP");
+      return e && std::string(e) == "simt";
+    }();
+    if (C == 32 && !simt)
+      up_prune_tc(c, S, X(k), cs() + o.nb[k], o.N[k], o.N[k + 1], L, dst);
+    else
+      up_prune(c, S, X(k), par() + o.nb[k + 1], key() + o.nb[k + 1], o.N[k + 1], C, L, dst);
+  }
+
   void kmap(int d) {
     kernel_map(c, key() + o.nb[d], o.N[d], d, nbr(d));
     if (c->debug) dbg_copy(c, nm("nbr", d), nbr(d), size_t(o.N[d]) * 27 * 4);
@@ -404,7 +417,7 @@ struct Net {
       dbgF(nm("ha", d), h, n, C);
       conv3(c, h, nullptr, C, n, nbr(d - 1), s.b, 1, F(d - 1), nullptr, s.k_s, nullptr, S);   // conv_b + k_s*F skip
       dbgF(nm("S", d), S, n, C);
-      up_prune(c, S, X(d - 1), par() + o.nb[d], key() + o.nb[d], o.N[d], C, s.up, F(d));       // Eq.9
+      up(d - 1, S, s.up, F(d));  // Eq.9
       dbgF(nm("F", d), F(d), o.N[d], C);
       return F(d);
     }
@@ -438,7 +451,7 @@ struct Net {
     const int8_t* cur = Hk;
     for (int k = D; k < d; ++k) {
       int8_t* dst = (k - D) % 2 == 0 ? ua : ub;
-      up_prune(c, cur, X(k), par() + o.nb[k + 1], key() + o.nb[k + 1], o.N[k + 1], C, dp.up[k - D], dst);
+      up(k, cur, dp.up[k - D], dst);
       dbgF(nm("Fp", d, k + 1), dst, o.N[k + 1], C);
       cur = dst;
     }
