@@ -151,11 +151,64 @@ def run_reference(args, rank, world):
 
 
 # --------------------------------------------------------------------------------------
+# multi-GPU plumbing: frames shard by index (no data-path collective); one all_gather of
+# per-rank stats; whole-job rate = all frames / max-over-ranks device time (weak scaling)
+# --------------------------------------------------------------------------------------
+
+STAT_FIELDS = ("frames", "points", "voxels", "bytes", "enc_ns", "dec_ns", "mismatch", "tot_ns", "e2e_ns")
+
+
+def shard_frames(rank: int, world: int, batch: int):
+    """Frame indices of this rank: a contiguous block of `batch` frames of the sequence."""
+    return list(range(rank * batch, (rank + 1) * batch))
+
+
+def rank_stats(B, npts, nvox, nbytes, enc_ms, dec_ms, parity, e2e_ms):
+    return np.array([B, npts, nvox, nbytes, int(enc_ms * 1e6), int(dec_ms * 1e6), int(parity is False),
+                     int((enc_ms + dec_ms) * 1e6), int(e2e_ms * 1e6)], np.int64)
+
+
+def gather_stats(dist, stats, device, world):
+    """all_gather of the int64 stats vector (NCCL on the GPU path, gloo in CPU tests)."""
+    if not dist:
+        return stats[None]
+    import torch
+    t = torch.from_numpy(stats).to(device)
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return np.stack([a.cpu().numpy() for a in out])
+
+
+def aggregate(allst, K):
+    frames = int(allst[:, 0].sum()) * K
+    t_max_ms = float(allst[:, 7].max()) / 1e6
+    return {"frames": frames, "t_max_ms": t_max_ms, "value": frames / (t_max_ms / 1e3),
+            "enc_fps": frames / (float(allst[:, 4].max()) / 1e9), "dec_fps": frames / (float(allst[:, 5].max()) / 1e9),
+            "points": int(allst[:, 1].sum()) * K, "voxels": int(allst[:, 2].sum()) * K,
+            "bytes": int(allst[:, 3].sum()) * K, "mismatch": int(allst[:, 6].sum()),
+            "e2e_ms_max": float(allst[:, 8].max()) / 1e6}
+
+
+# --------------------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------------------
 
 ALU_PEAK_NOTE = ("B200 integer issue peak = 148 SM x 4 SMSP x 32 lanes x 1 instr/clk x sm_max clock "
                  "(DESIGN.md §5)")
+# Algorithmic integer ops per coded node of the predictor + integer softmax (DESIGN.md §5):
+# hidden layer C*H/4 dp4a (C = H = 32) + 12 ops per symbol (logit requant mul-add, shift,
+# saturate; max; delta; LUT index/load/select; sum; scale multiply; quotient; correction;
+# accumulate) x 255; the decoder adds the prefix-sum store (13 per symbol).
+ALU_OPS_PER_NODE = {"head_enc": 32 * 32 / 4 + 12 * 255, "head_dec": 32 * 32 / 4 + 13 * 255}
+
+
+def measured_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(kernel)
+    except Exception:
+        return None
 
 
 def run_ours(args, rank, world, dist):
@@ -170,7 +223,7 @@ def run_ours(args, rank, world, dist):
     L = cfg.bit_depth
     B = args.batch
     mb = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18).to_bytes()
-    frames, offs = make_inputs(cfg, B, rank * B)
+    frames, offs = make_inputs(cfg, B, shard_frames(rank, world, B)[0])
     npts = offs[-1]
     host_xyz = torch.from_numpy(np.concatenate(frames).astype(np.int32)).pin_memory()
     codec = pcc.Codec(mb, dev, stream)
@@ -277,53 +330,36 @@ def run_ours(args, rank, world, dist):
         coded_per_step += sum(cnt[4:L])
 
     # ---- gather per-rank stats (the only collective) ----
-    stats = np.array([B, npts, nvox, nbytes, int(enc_ms * 1e6), int(dec_ms * 1e6), int(parity is False),
-                      int(tot_ms * 1e6)], np.int64)
-    if dist:
-        t = torch.from_numpy(stats).to(f"cuda:{dev}")
-        allst = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(allst, t)
-        allst = np.stack([a.cpu().numpy() for a in allst])
-        e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-        e2e_ms_max = float(e2e_t.item())
-    else:
-        allst = stats[None]
-        e2e_ms_max = e2e_ms
+    stats = rank_stats(B, npts, nvox, nbytes, enc_ms, dec_ms, parity, e2e_ms)
+    allst = gather_stats(dist, stats, f"cuda:{dev}", world)
     if rank != 0:
         return
-    frames_tot = int(allst[:, 0].sum()) * K
-    t_max_ms = float(allst[:, 7].max()) / 1e6
-    value = frames_tot / (t_max_ms / 1e3)
-    enc_fps = frames_tot / (float(allst[:, 4].max()) / 1e9)
-    dec_fps = frames_tot / (float(allst[:, 5].max()) / 1e9)
-    pts_tot = int(allst[:, 1].sum()) * K
+    agg = aggregate(allst, K)
+    frames_tot, t_max_ms, value = agg["frames"], agg["t_max_ms"], agg["value"]
+    enc_fps, dec_fps, pts_tot, e2e_ms_max = agg["enc_fps"], agg["dec_fps"], agg["points"], agg["e2e_ms_max"]
 
-    # ---- roofline of the dominant kernel category ----
+    # ---- roofline of the dominant kernel category (DESIGN.md §5) ----
     pk, pk_src = peaks()
     top = max(prof.items(), key=lambda kv: kv[1]["ms_per_step"]) if prof else (None, None)
     roof = None
     if top[0]:
         name, v = top
-        sm_max = float(pk.get("sm_max_mhz", 1965.0))
-        if name in ("head_enc", "head_dec", "rans_enc", "rans_dec"):
-            # ALU-bound: algorithmic integer ops per node
-            C = H = 32
-            ops_per_node = {"head_enc": (C * H + H * 255) / 4 + 255 * 8,
-                            "head_dec": (C * H + H * 255) / 4 + 255 * 9,
-                            "rans_enc": 30, "rans_dec": 40}[name]
-            coded_nodes = coded_per_step
-            achieved = coded_nodes * ops_per_node / (v["ms_per_step"] / 1e3) / 1e12
+        sec = v["ms_per_step"] / 1e3
+        traffic = measured_traffic(name)
+        if name in ALU_OPS_PER_NODE:
+            # integer-ALU bound: algorithmic ops per coded node x coded nodes per step
+            sm_max = float(pk.get("sm_max_mhz", 1965.0))
+            achieved = coded_per_step * ALU_OPS_PER_NODE[name] / sec / 1e12
             peak = 148 * 4 * 32 * sm_max * 1e6 / 1e12
             roof = {"kernel": name, "bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                    "frac": achieved / peak, "traffic": None, "peak_src": ALU_PEAK_NOTE,
-                    "share_of_step": v["ms_per_step"] / prof_total}
+                    "frac": achieved / peak, "traffic": traffic, "peak_src": ALU_PEAK_NOTE,
+                    "launches_per_step": v["launches_per_step"], "share_of_step": v["ms_per_step"] / prof_total}
         else:
-            achieved = v["bytes_per_step"] / (v["ms_per_step"] / 1e3) / 1e9
+            achieved = v["bytes_per_step"] / sec / 1e9
             peak = float(pk["hbm_gbs"])
             roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": None, "peak_src": pk_src,
-                    "share_of_step": v["ms_per_step"] / prof_total}
+                    "frac": achieved / peak, "traffic": traffic, "peak_src": pk_src + " copy bandwidth",
+                    "launches_per_step": v["launches_per_step"], "share_of_step": v["ms_per_step"] / prof_total}
 
     # ---- CPU baseline: the oracle on a bounded sample of the same workload ----
     cpu = None
@@ -345,6 +381,7 @@ def run_ours(args, rank, world, dist):
         "parity_sample_frame0": parity, "wall_s_timed_region": t_wall,
         "gpu_launches": gpu_launches,
         "e2e": {"value": B * world / (e2e_ms_max / 1e3) if e2e_ms_max else None, "unit": UNIT,
+                "scope": "pcc_encode_batch_host + pcc_decode_batch_host (pinned host in/out), max over ranks",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "clocks": clk.summary(),
         "roofline": roof,
@@ -359,7 +396,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")

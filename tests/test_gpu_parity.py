@@ -300,3 +300,36 @@ def test_errors(pcc, ctx):
     # the context is still usable after errors
     good, _ = gpu_encode(pcc, ctx, m, [pts], 10)
     assert good[0] == bs
+
+
+# ---------------------------------------------------------------------------------------
+# alternate kernel variants (A/B baselines selected by environment) stay bit-exact
+# ---------------------------------------------------------------------------------------
+
+_ALT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from oracle import oracle as O
+from paper_2603_25260_b200 import inputs as I, pcc
+mb = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18).to_bytes()
+om = O.Model(mb)
+codec = pcc.Codec(mb, 0)
+for pts, L in [(I.make_frame(I.CFG1), 12), (I.random_cloud(3000, 10, 5, spread=0.3), 10)]:
+    x = torch.from_numpy(pts).cuda()
+    out, oo = codec.encode_frames(x, [0, len(pts)], L)
+    assert out[:oo[1]].cpu().numpy().tobytes() == O.encode(om, pts, L)
+    xyz, no = codec.decode_frames(out, oo, len(pts))
+    assert np.array_equal(xyz[:no[1]].cpu().numpy(), O.decode(om, O.encode(om, pts, L))[0])
+print("ALT-OK")
+"""
+
+
+@pytest.mark.parametrize("env", [{"PCC_UP": "tc"}, {"PCC_HEAD": "simt", "PCC_CONV": "simt"}])
+def test_alternate_kernels_bit_exact(pcc, env):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _ALT.format(root=root)], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert "ALT-OK" in r.stdout, r.stdout + r.stderr
