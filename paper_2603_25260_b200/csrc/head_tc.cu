@@ -23,7 +23,7 @@ namespace {
 
 constexpr int TILE = 128;
 constexpr uint32_t IDESC = tc::idesc_i8(128, 256);
-constexpr int STG = 258;  // staged cdf row stride in u16 (516 B: conflict-free)
+constexpr int STG = 264;  // staged cdf row stride in u16 (528 B: 16-B aligned, STS.128/LDS.128 conflict-free)
 
 __device__ __forceinline__ int32_t rq8(int32_t acc, RQ q) {
   int64_t v = int64_t(acc) * int64_t(acc >= 0 ? q.mp : q.mn);
@@ -293,15 +293,16 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         tc::tmem_wait_ld();
         pchunk(v);
 #pragma unroll
-        for (int k = 0; k < 16; k += 2) {
-          const int i = 64 * q + ch * 16 + k;
-          uint32_t c2[2];
+        for (int k8 = 0; k8 < 16; k8 += 8) {  // 8 entries -> one 16-byte shared store
+          uint32_t w[4];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            c2[u] = run;  // quarter-local prefix (< 2^16)
-            run += v[k + u];
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t c0 = run;  // quarter-local prefix (< 2^16)
+            run += v[k8 + 2 * u];
+            w[u] = (c0 & 0xffffu) | (run << 16);
+            run += v[k8 + 2 * u + 1];
           }
-          *reinterpret_cast<uint32_t*>(srow + i) = (c2[0] & 0xffffu) | (c2[1] << 16);
+          *reinterpret_cast<uint4*>(srow + 64 * q + ch * 16 + k8) = make_uint4(w[0], w[1], w[2], w[3]);
         }
       }
       if (q == 3) run -= 1u;  // padding column 255
@@ -318,22 +319,29 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         rowi[r * 8 + 5] = istar;
       }
       __syncthreads();
-      // coalesced write-out: 4 rows per iteration, 128 u16 pairs per row
+      // coalesced write-out: 16 rows per iteration, 32 threads x 16 bytes per 512-byte row;
+      // adds the quarter offset and, after the first argmax, the leftover
       const uint32_t rows_here = (n - tile * TILE) < uint32_t(TILE) ? (n - tile * TILE) : uint32_t(TILE);
-      const uint32_t pr = uint32_t(tid) & 127u, sub = uint32_t(tid) >> 7;
-      for (uint32_t rb = 0; rb < rows_here; rb += 4) {
+      const uint32_t j = uint32_t(tid) & 31u, sub = uint32_t(tid) >> 5;
+      for (uint32_t rb = 0; rb < rows_here; rb += 16) {
         const uint32_t rr = rb + sub;
         if (rr < rows_here) {
-          const uint32_t i0 = 2u * pr;
           const int32_t* ri = rowi + rr * 8;
-          const uint32_t off = uint32_t(ri[i0 >> 6]);
+          const uint32_t off = uint32_t(ri[j >> 3]);
           const uint32_t left = uint32_t(ri[4]);
           const int isr = ri[5];
-          const uint32_t pair = *reinterpret_cast<const uint32_t*>(stage + rr * STG + i0);
-          const uint32_t c0 = (pair & 0xffffu) + off + (int(i0) > isr ? left : 0u);
-          uint32_t c1 = (pair >> 16) + off + (int(i0 + 1) > isr ? left : 0u);
-          if (i0 + 1 >= uint32_t(NCODE)) c1 = 0xffffu;
-          reinterpret_cast<uint32_t*>(cdf + size_t(tile * TILE + rr) * 256)[pr] = (c0 & 0xffffu) | (c1 << 16);
+          const uint4 g = *reinterpret_cast<const uint4*>(stage + rr * STG + 8 * j);
+          const uint32_t in[4] = {g.x, g.y, g.z, g.w};
+          uint32_t o[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i0 = int(8 * j) + 2 * u;
+            const uint32_t c0 = (in[u] & 0xffffu) + off + (i0 > isr ? left : 0u);
+            uint32_t c1 = (in[u] >> 16) + off + (i0 + 1 > isr ? left : 0u);
+            if (i0 + 1 >= NCODE) c1 = 0xffffu;
+            o[u] = (c0 & 0xffffu) | (c1 << 16);
+          }
+          reinterpret_cast<uint4*>(cdf + size_t(tile * TILE + rr) * 256)[j] = make_uint4(o[0], o[1], o[2], o[3]);
         }
       }
     }
