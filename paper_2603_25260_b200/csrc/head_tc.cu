@@ -63,15 +63,15 @@ constexpr int NT = 512;
 struct SmemLayout {
   static constexpr int B = 0;           // W2 operand 256 x 32 (8 KB)
   static constexpr int A = 8192;        // a operand 128 x 32 (4 KB)
-  static constexpr int LUT = 12288;     // 4 KB
-  static constexpr int B2 = 16384;      // 1 KB
-  static constexpr int W1 = 17408;      // <= 1 KB
-  static constexpr int B1 = 18432;      // <= 256 B
-  static constexpr int MBAR = 18688;
-  static constexpr int THOLD = 18696;
-  static constexpr int RED = 18704;     // [4][128] x (a, b) int32 = 4 KB
-  static constexpr int ROWI = 22800;    // [128] x 8 int32 = 4 KB
-  static constexpr int STAGE = 26896;   // decoder: 128 x STG u16 (66 KB)
+  static constexpr int LUT = 12288;     // 1024 entries + LUT[1024] = 0 sentinel (4 KB + 16 B)
+  static constexpr int B2 = 16400;      // 1 KB
+  static constexpr int W1 = 17424;      // <= 1 KB
+  static constexpr int B1 = 18448;      // <= 256 B
+  static constexpr int MBAR = 18704;
+  static constexpr int THOLD = 18712;
+  static constexpr int RED = 18720;     // [4][128] x (a, b) int32 = 4 KB
+  static constexpr int ROWI = 22816;    // [128] x 8 int32 = 4 KB
+  static constexpr int STAGE = 26912;   // decoder: 128 x STG u16 (66 KB)
   static constexpr int END = STAGE + TILE * STG * 2;
 };
 
@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   }
   for (int k = tid; k < 1024; k += NT) reinterpret_cast<uint32_t*>(sA)[k] = 0u;  // K padding stays 0
   for (int k = tid; k < 1024; k += NT) sLut[k] = lut[k];
+  if (tid == 0) sLut[1024] = 0u;  // delta >= 4096 (16 nats): e = 0 (reading Q20)
   for (int k = tid; k < 256; k += NT) sb2[k] = b2[k];
   for (int k = tid; k < H * CW; k += NT) sW1[k] = reinterpret_cast<const int32_t*>(W1)[k];
   for (int k = tid; k < H; k += NT) sb1[k] = b1[k];
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
 
     // ---- pass 1: max of z (the requant is monotone non-decreasing, m >= 0, so
     //      max_i lq(z_i) = lq(max_i z_i)) ----
-    int32_t zmax = INT32_MIN;
+    int32_t zmax = INT32_MIN, zmin = INT32_MAX;
 #pragma unroll 1
     for (int ch = 0; ch < 4; ++ch) {
       uint32_t v[16];
@@ -174,13 +175,21 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const int i = 64 * q + ch * 16 + k;
-        if (i < NCODE) zmax = max(zmax, int32_t(v[k]) + sb2[i]);
+        if (i < NCODE) {
+          zmax = max(zmax, int32_t(v[k]) + sb2[i]);
+          zmin = min(zmin, int32_t(v[k]) + sb2[i]);
+        }
       }
     }
     red[(q * TILE + r) * 2] = zmax;
+    red[(q * TILE + r) * 2 + 1] = zmin;
     __syncthreads();
-    const int32_t mu = lq8(max(max(red[r * 2], red[(TILE + r) * 2]), max(red[(2 * TILE + r) * 2], red[(3 * TILE + r) * 2])),
-                           rql);
+    const int32_t zmx = max(max(red[r * 2], red[(TILE + r) * 2]), max(red[(2 * TILE + r) * 2], red[(3 * TILE + r) * 2]));
+    const int32_t zmn =
+        min(min(red[r * 2 + 1], red[(TILE + r) * 2 + 1]), min(red[(2 * TILE + r) * 2 + 1], red[(3 * TILE + r) * 2 + 1]));
+    const int32_t mu = lq8(zmx, rql);
+    // the whole row avoids saturation: l = low word of the 64-bit shift, no selects
+    const bool nosat = zmx <= zsat_hi && zmn >= zsat_lo;
     // ---- pass 2: Q8 logit, e = LUT[delta >> 2] (0 beyond 16 nats), local sum and
     //      local first index with delta == 0 (e stored back into TMEM) ----
     uint32_t ssum = 0;
@@ -197,13 +206,15 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         const int i = 64 * q + ch * 16 + k;
         const int32_t zz = int32_t(v[k]) + sb2[i];
         // lq8(zz) without the 64-bit clamp: saturation is decided in the z domain and
-        // selected (branch-free) over the low word of the 64-bit shift
+        // selected (branch-free) over the low word of the 64-bit shift; rows whose
+        // [zmin, zmax] lies inside the thresholds skip the selects
         int32_t lv = int32_t((int64_t(zz) * lm + lhalf) >> lr);
-        lv = zz > zsat_hi ? (1 << 24) : lv;
-        lv = zz < zsat_lo ? -(1 << 24) : lv;
+        if (!nosat) {
+          lv = zz > zsat_hi ? (1 << 24) : lv;
+          lv = zz < zsat_lo ? -(1 << 24) : lv;
+        }
         const uint32_t dl = uint32_t(mu - lv);
-        const uint32_t e0 = sLut[min(dl, 4095u) >> 2];  // unconditional load: no branch
-        const uint32_t e = dl < 4096u ? e0 : 0u;
+        const uint32_t e = sLut[min(dl >> 2, 1024u)];  // LUT[1024] = 0: delta >= 4096
         if (dl == 0u) ist = min(ist, i);  // i increases: the first index wins
         v[k] = e;
       }
@@ -256,18 +267,24 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         tmem_ld16(taddr + ch * 16, v);
         tc::tmem_wait_ld();
         pchunk(v);
+        uint32_t cs16 = 0;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int i = 64 * q + ch * 16 + k;
-          tot += v[k];
-          cum += (i < sym) ? v[k] : 0u;
-          fq = (i == sym) ? v[k] : fq;
+        for (int k = 0; k < 16; ++k) cs16 += v[k];
+        tot += cs16;
+        const int i0 = 64 * q + ch * 16;
+        if (sym >= i0 + 16) {
+          cum += cs16;  // the whole chunk precedes the symbol
+        } else if (sym >= i0) {  // the chunk holding the symbol (one per row)
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            cum += (i0 + k < sym) ? v[k] : 0u;
+            fq = (i0 + k == sym) ? v[k] : fq;
+          }
         }
       }
       if (q == 3) tot -= 1u;  // the padding column 255 (e = 0 -> p = 1) is not a symbol
       __syncthreads();  // Ssum reads done
       red[(q * TILE + r) * 2] = int32_t(tot);
-      red[(q * TILE + r) * 2 + 1] = int32_t(cum | (fq << 16));  // cum < 2^16 per quarter? use rowi
       rowi[r * 8 + q] = int32_t(cum);
       rowi[r * 8 + 4 + q] = int32_t(fq);
       __syncthreads();
