@@ -218,116 +218,178 @@ def run_ours(args, rank, world, dist):
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
-    stream = torch.cuda.Stream(dev)
     cfg = I.CFG2
     L = cfg.bit_depth
     B = args.batch
+    S = max(1, min(args.streams, B))
     mb = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18).to_bytes()
     frames, offs = make_inputs(cfg, B, shard_frames(rank, world, B)[0])
     npts = offs[-1]
     host_xyz = torch.from_numpy(np.concatenate(frames).astype(np.int32)).pin_memory()
-    codec = pcc.Codec(mb, dev, stream)
-    with torch.cuda.stream(stream):
-        d_xyz = host_xyz.to(f"cuda:{dev}", non_blocking=True)
-        cap = sum(pcc.pcc_encode_bound(offs[i + 1] - offs[i], L) + 4 for i in range(B))
-        d_bs = torch.empty(cap, dtype=torch.uint8, device=f"cuda:{dev}")
-        d_out = torch.empty((npts, 3), dtype=torch.int32, device=f"cuda:{dev}")
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
-    stream.synchronize()
+    model = pcc.pcc_model_load(mb, dev)
+    main = torch.cuda.Stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
 
-    def step(evs=None):
-        if evs:
-            evs[0].record(stream)
-        oo = pcc.pcc_encode_batch(codec.ctx, codec.model, d_xyz, offs, L, d_bs, cap)
-        if evs:
-            evs[1].record(stream)
-        no = pcc.pcc_decode_batch(codec.ctx, codec.model, d_bs, oo, d_out, npts)
-        if evs:
-            evs[2].record(stream)
-        return oo, no
+    class Lane:
+        """One of S concurrent codec instances (own ctx + stream) on a slice of the frames."""
+
+        def __init__(self, f0, f1):
+            self.stream = torch.cuda.Stream(dev)
+            self.ctx = pcc.pcc_ctx_create(dev, self.stream.cuda_stream)
+            self.offs = [o - offs[f0] for o in offs[f0:f1 + 1]]
+            self.n = self.offs[-1]
+            with torch.cuda.stream(self.stream):
+                self.xyz = host_xyz[offs[f0]:offs[f1]].to(f"cuda:{dev}", non_blocking=True)
+                self.cap = sum(pcc.pcc_encode_bound(self.offs[i + 1] - self.offs[i], L) + 4
+                               for i in range(len(self.offs) - 1))
+                self.bs = torch.empty(self.cap, dtype=torch.uint8, device=f"cuda:{dev}")
+                self.out = torch.empty((self.n, 3), dtype=torch.int32, device=f"cuda:{dev}")
+            self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+        def run(self, start_ev=None):
+            if start_ev is not None:
+                self.stream.wait_event(start_ev)
+            self.oo = pcc.pcc_encode_batch(self.ctx, model, self.xyz, self.offs, L, self.bs, self.cap)
+            self.ev[0].record(self.stream)
+            self.no = pcc.pcc_decode_batch(self.ctx, model, self.bs, self.oo, self.out, self.n)
+            self.ev[1].record(self.stream)
+
+    cuts = [B * k // S for k in range(S + 1)]
+    lanes = [Lane(cuts[k], cuts[k + 1]) for k in range(S)]
+    torch.cuda.synchronize(dev)
+    import threading as _th
+
+    def step(timed=False):
+        """Encode + decode all B frames: the S lanes run concurrently (one host thread each)."""
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(main)
+        ths = [_th.Thread(target=ln.run, args=(start,)) for ln in lanes[1:]]
+        for t_ in ths:
+            t_.start()
+        lanes[0].run(start)
+        for t_ in ths:
+            t_.join()
+        end = torch.cuda.Event(enable_timing=True)
+        for ln in lanes:
+            main.wait_event(ln.ev[1])
+        end.record(main)
+        return start, end
 
     for _ in range(args.warmup):
-        oo, no = step()
-    stream.synchronize()
-    nvox = no[-1]
-    nbytes = oo[-1]
+        step()
+    torch.cuda.synchronize(dev)
+    nvox = sum(ln.no[-1] for ln in lanes)
+    nbytes = sum(ln.oo[-1] for ln in lanes)
 
     # parity sample (outside the timed region): frame 0 vs the CPU oracle, and round trip
     parity = None
     if not args.no_parity and rank == 0:
         from oracle import oracle as O
-        got = d_bs[oo[0]:oo[1]].cpu().numpy().tobytes()
+        l0 = lanes[0]
+        got = l0.bs[l0.oo[0]:l0.oo[1]].cpu().numpy().tobytes()
         want = O.encode(O.Model(mb), frames[0], L)
-        dec = d_out[no[0]:no[1]].cpu().numpy()
+        dec = l0.out[l0.no[0]:l0.no[1]].cpu().numpy()
         ref, _ = O.decode(O.Model(mb), want)
         parity = bool(got == want and np.array_equal(dec, ref))
 
     # ---- timed region: K steps, L2 flushed between steps (outside the events) ----
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    evs = []
     with Clocks(dev) as clk:
         t_wall0 = time.perf_counter()
         for k in range(K):
-            with torch.cuda.stream(stream):
+            with torch.cuda.stream(main):
                 flush.zero_()
-            oo, no = step(evs[k])
-        stream.synchronize()
+            start, end = step(True)
+            evs.append((start, end, [(ln.ev[0], ln.ev[1]) for ln in lanes]))
+            torch.cuda.synchronize(dev)  # lanes' events are reused next step
+            evs[-1] = (start.elapsed_time(end), max(start.elapsed_time(a_) for a_, _ in evs[-1][2]),
+                       max(a_.elapsed_time(b_) for a_, b_ in evs[-1][2]))
         t_wall = time.perf_counter() - t_wall0
     torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()
-    enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
-    dec_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
-    tot_ms = enc_ms + dec_ms
+    tot_ms = sum(e[0] for e in evs)
+    enc_ms = sum(e[1] for e in evs)  # start -> last lane's encode done
+    dec_ms = sum(e[2] for e in evs)  # slowest lane's decode
+    # own-kernel launches per step (counted by the library, per ctx)
+    step()
+    torch.cuda.synchronize(dev)
+    gpu_launches = 0
+    for ln in lanes:
+        pcc.pcc_encode_batch(ln.ctx, model, ln.xyz, ln.offs, L, ln.bs, ln.cap)
+        gpu_launches += pcc.pcc_ctx_launch_count(ln.ctx)
+        pcc.pcc_decode_batch(ln.ctx, model, ln.bs, ln.oo, ln.out, ln.n)
+        gpu_launches += pcc.pcc_ctx_launch_count(ln.ctx)
+    gpu_launches *= K
 
-    # own-kernel launches per step: count one encode and one decode separately
-    pcc.pcc_encode_batch(codec.ctx, codec.model, d_xyz, offs, L, d_bs, cap)
-    enc_l = pcc.pcc_ctx_launch_count(codec.ctx)
-    pcc.pcc_decode_batch(codec.ctx, codec.model, d_bs, oo, d_out, npts)
-    dec_l = pcc.pcc_ctx_launch_count(codec.ctx)
-    gpu_launches = K * (enc_l + dec_l)
-
-    # ---- profiled pass (CUDA events around every launch, same stream) ----
-    pcc.pcc_ctx_set_profile(codec.ctx, True)
-    KP = max(1, min(K, 5))
+    # ---- profiled pass (CUDA events around every launch, same streams; lanes serial) ----
+    KP = max(1, min(K, 3))
+    for ln in lanes:
+        pcc.pcc_ctx_set_profile(ln.ctx, True)
     for _ in range(KP):
-        with torch.cuda.stream(stream):
+        with torch.cuda.stream(main):
             flush.zero_()
-        step()
+        torch.cuda.synchronize(dev)
+        for ln in lanes:
+            ln.run()
+        torch.cuda.synchronize(dev)
     prof = {}
-    for cname in pcc.pcc_ctx_profile_categories(codec.ctx):
-        ms, nl, nb = pcc.pcc_ctx_profile_get(codec.ctx, cname)
-        prof[cname] = {"ms_per_step": ms / KP, "launches_per_step": nl / KP, "bytes_per_step": nb / KP}
-    pcc.pcc_ctx_set_profile(codec.ctx, False)
+    for ln in lanes:
+        for cname in pcc.pcc_ctx_profile_categories(ln.ctx):
+            ms, nl, nb = pcc.pcc_ctx_profile_get(ln.ctx, cname)
+            d = prof.setdefault(cname, {"ms_per_step": 0.0, "launches_per_step": 0.0, "bytes_per_step": 0.0})
+            d["ms_per_step"] += ms / KP
+            d["launches_per_step"] += nl / KP
+            d["bytes_per_step"] += nb / KP
+        pcc.pcc_ctx_set_profile(ln.ctx, False)
     prof_total = sum(v["ms_per_step"] for v in prof.values())
 
-    # ---- e2e through the host-buffer C ABI (H2D inputs + D2H results inside) ----
-    h_bs = torch.empty(cap, dtype=torch.uint8).pin_memory()
-    h_out = torch.empty((npts, 3), dtype=torch.int32).pin_memory()
+    # ---- e2e through the host-buffer C ABI (H2D inputs + D2H results inside), one lane
+    #      per host thread, same concurrency as the device-resident measurement ----
+    for ln in lanes:
+        ln.h_bs = torch.empty(ln.cap, dtype=torch.uint8).pin_memory()
+        ln.h_out = torch.empty((ln.n, 3), dtype=torch.int32).pin_memory()
+        ln.h_xyz = host_xyz[offs[cuts[lanes.index(ln)]]:offs[cuts[lanes.index(ln) + 1]]]
+
+    def e2e_lane(ln):
+        ln.oo_h = pcc.pcc_encode_batch_host(ln.ctx, model, ln.h_xyz, ln.offs, L, ln.h_bs, ln.cap)
+        ln.no_h = pcc.pcc_decode_batch_host(ln.ctx, model, ln.h_bs, ln.oo_h, ln.h_out, ln.n)
+
     KE = max(1, min(K, 5))
     e2e_ms = 0.0
-    h2d = d2h = 0
     for k in range(KE + 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        oo_h = pcc.pcc_encode_batch_host(codec.ctx, codec.model, host_xyz, offs, L, h_bs, cap)
-        no_h = pcc.pcc_decode_batch_host(codec.ctx, codec.model, h_bs, oo_h, h_out, npts)
-        e1.record(stream)
-        stream.synchronize()
-        if k > 0:  # first is a warm-up of the e2e buffers
+        e0.record(main)
+        for ln in lanes:
+            ln.stream.wait_event(e0)
+        ths = [_th.Thread(target=e2e_lane, args=(ln,)) for ln in lanes]
+        for t_ in ths:
+            t_.start()
+        for t_ in ths:
+            t_.join()
+        for ln in lanes:
+            done = torch.cuda.Event()
+            done.record(ln.stream)
+            main.wait_event(done)
+        e1.record(main)
+        torch.cuda.synchronize(dev)
+        if k > 0:  # the first pass sizes the e2e buffers
             e2e_ms += e0.elapsed_time(e1)
-        h2d = npts * 12 + oo_h[-1]
-        d2h = oo_h[-1] + no_h[-1] * 12
     e2e_ms /= KE
+    h2d = sum(ln.n * 12 + ln.oo_h[-1] for ln in lanes)
+    d2h = sum(ln.oo_h[-1] + ln.no_h[-1] * 12 for ln in lanes)
+    d_xyz_list = [(ln.xyz, ln.offs) for ln in lanes]
 
     # coded symbols per step (levels R..L-1 of every frame), for per-node op counts
     coded_per_step = 0
-    for i in range(B):
-        cnt = pcc.pcc_build_octree(codec.ctx, d_xyz[offs[i]:offs[i + 1]], offs[i + 1] - offs[i], L)
-        coded_per_step += sum(cnt[4:L])
+    for xyz_l, offs_l in d_xyz_list:
+        for i in range(len(offs_l) - 1):
+            cnt = pcc.pcc_build_octree(lanes[0].ctx, xyz_l[offs_l[i]:offs_l[i + 1]], offs_l[i + 1] - offs_l[i], L)
+            coded_per_step += sum(cnt[4:L])
 
     # ---- gather per-rank stats (the only collective) ----
     stats = rank_stats(B, npts, nvox, nbytes, enc_ms, dec_ms, parity, e2e_ms)
@@ -374,6 +436,7 @@ def run_ours(args, rank, world, dist):
         "ms_per_step": t_max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int8 x int8 -> int32 (integer-only)", "data": "synthetic",
         "config": {"workload": WORKLOAD, "frames_per_gpu_per_step": B, "global_batch": B * world,
+                   "lanes_per_gpu": S, "frames_per_launch": B // S,
                    "points_per_frame": npts / B, "voxels_per_frame": nvox / B, "parallelism": f"frames/dp{world}",
                    "l2": "flushed between steps (256 MiB write, outside the events)"},
         "enc_fps": enc_fps, "dec_fps": dec_fps, "points_per_s": pts_tot / (t_max_ms / 1e3),
@@ -397,6 +460,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--streams", type=int, default=2, help="concurrent codec lanes (ctx + stream) per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
