@@ -460,7 +460,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=256)
-    ap.add_argument("--streams", type=int, default=2, help="concurrent codec lanes (ctx + stream) per GPU")
+    ap.add_argument("--streams", type=int, default=4, help="concurrent codec lanes (ctx + stream) per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")

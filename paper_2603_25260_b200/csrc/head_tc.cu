@@ -63,19 +63,22 @@ constexpr int NT = 512;
 struct SmemLayout {
   static constexpr int B = 0;           // W2 operand 256 x 32 (8 KB)
   static constexpr int A = 8192;        // a operand 128 x 32 (4 KB)
-  static constexpr int LUT = 12288;     // 1024 entries + LUT[1024] = 0 sentinel (4 KB + 16 B)
-  static constexpr int B2 = 16400;      // 1 KB
-  static constexpr int W1 = 17424;      // <= 1 KB
-  static constexpr int B1 = 18448;      // <= 256 B
-  static constexpr int MBAR = 18704;
-  static constexpr int THOLD = 18712;
-  static constexpr int RED = 18720;     // [4][128] x (a, b) int32 = 4 KB
-  static constexpr int ROWI = 22816;    // [128] x 8 int32 = 4 KB
-  static constexpr int STAGE = 26912;   // decoder: 128 x STG u16 (66 KB)
+  // exp table indexed by delta itself: LUT4[j] = LUT[j >> 2] for j < 4096, LUT4[4096] = 0
+  static constexpr int LUT = 12288;              // 4097 x u32 (16 KB + 4 B)
+  static constexpr int B2 = LUT + 16400;         // 1 KB
+  static constexpr int W1 = B2 + 1024;           // <= 1 KB
+  static constexpr int B1 = W1 + 1024;           // <= 256 B
+  static constexpr int MBAR = B1 + 256;
+  static constexpr int THOLD = MBAR + 8;
+  static constexpr int RED = MBAR + 16;          // [4][128] x (a, b) int32 = 4 KB
+  static constexpr int ROWI = RED + 4096;        // [128] x 8 int32 = 4 KB
+  static constexpr int STAGE = ROWI + 4096;      // decoder: 128 x STG u16 (66 KB)
   static constexpr int END = STAGE + TILE * STG * 2;
 };
 
-template <int C, int H, int MODE>
+// SAT = false when the model proves |z| can never reach the logit saturation thresholds
+// (checked at load from |b2| + 128 * sum|W2|): no min tracking, no saturation selects.
+template <int C, int H, int MODE, bool SAT>
 __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F, uint32_t n,
                                                    const int8_t* __restrict__ W1, const int32_t* __restrict__ b1, RQ rq1,
                                                    const int8_t* __restrict__ W2, const int32_t* __restrict__ b2, RQ rql,
@@ -107,8 +110,8 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     *reinterpret_cast<uint32_t*>(sB + tc::kmaj_off(rr, 4 * w)) = v;
   }
   for (int k = tid; k < 1024; k += NT) reinterpret_cast<uint32_t*>(sA)[k] = 0u;  // K padding stays 0
-  for (int k = tid; k < 1024; k += NT) sLut[k] = lut[k];
-  if (tid == 0) sLut[1024] = 0u;  // delta >= 4096 (16 nats): e = 0 (reading Q20)
+  for (int k = tid; k < 4096; k += NT) sLut[k] = lut[k >> 2];
+  if (tid == 0) sLut[4096] = 0u;  // delta >= 4096 (16 nats): e = 0 (reading Q20)
   for (int k = tid; k < 256; k += NT) sb2[k] = b2[k];
   for (int k = tid; k < H * CW; k += NT) sW1[k] = reinterpret_cast<const int32_t*>(W1)[k];
   for (int k = tid; k < H; k += NT) sb1[k] = b1[k];
@@ -177,7 +180,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         const int i = 64 * q + ch * 16 + k;
         if (i < NCODE) {
           zmax = max(zmax, int32_t(v[k]) + sb2[i]);
-          zmin = min(zmin, int32_t(v[k]) + sb2[i]);
+          if (SAT) zmin = min(zmin, int32_t(v[k]) + sb2[i]);
         }
       }
     }
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         min(min(red[r * 2 + 1], red[(TILE + r) * 2 + 1]), min(red[(2 * TILE + r) * 2 + 1], red[(3 * TILE + r) * 2 + 1]));
     const int32_t mu = lq8(zmx, rql);
     // the whole row avoids saturation: l = low word of the 64-bit shift, no selects
-    const bool nosat = zmx <= zsat_hi && zmn >= zsat_lo;
+    const bool nosat = !SAT || (zmx <= zsat_hi && zmn >= zsat_lo);
     // ---- pass 2: Q8 logit, e = LUT[delta >> 2] (0 beyond 16 nats), local sum and
     //      local first index with delta == 0 (e stored back into TMEM) ----
     uint32_t ssum = 0;
@@ -209,12 +212,12 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         // selected (branch-free) over the low word of the 64-bit shift; rows whose
         // [zmin, zmax] lies inside the thresholds skip the selects
         int32_t lv = int32_t((int64_t(zz) * lm + lhalf) >> lr);
-        if (!nosat) {
+        if (SAT && !nosat) {
           lv = zz > zsat_hi ? (1 << 24) : lv;
           lv = zz < zsat_lo ? -(1 << 24) : lv;
         }
         const uint32_t dl = uint32_t(mu - lv);
-        const uint32_t e = sLut[min(dl >> 2, 1024u)];  // LUT[1024] = 0: delta >= 4096
+        const uint32_t e = sLut[min(dl, 4096u)];  // LUT4[4096] = 0: delta >= 4096
         if (dl == 0u) ist = min(ist, i);  // i increases: the first index wins
         v[k] = e;
       }
@@ -411,10 +414,10 @@ __global__ void __launch_bounds__(128) k_gemm_i8_test(const int8_t* __restrict__
   if (warp == 0) tc::tmem_dealloc<256>(tbase);
 }
 
-template <int C, int H, int MODE>
+template <int C, int H, int MODE, bool SAT>
 void launch_head(pcc_ctx c, const int8_t* F, uint32_t n, const DHead& L, const uint32_t* lut, const uint8_t* X,
                  uint32_t* cf, uint16_t* cdf, int8_t* a_dbg) {
-  auto kern = k_head_tc<C, H, MODE>;
+  auto kern = k_head_tc<C, H, MODE, SAT>;
   static bool attr = false;
   if (!attr) {
     PCC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemLayout::END));
@@ -435,8 +438,10 @@ void head_cdf_tc(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHe
   Prof p(c, mode == 0 ? "head_enc" : "head_dec", size_t(n) * (C + (mode == 0 ? 1 + 4 : 512)));
 #define PCC_HEAD(CC)                                                         \
   if (C == CC && H == CC) {                                                  \
-    if (mode == 0) launch_head<CC, CC, 0>(c, F, n, L, lut, X, cf, cdf, a_dbg); \
-    else launch_head<CC, CC, 1>(c, F, n, L, lut, X, cf, cdf, a_dbg);          \
+    if (mode == 0 && L.can_saturate) launch_head<CC, CC, 0, true>(c, F, n, L, lut, X, cf, cdf, a_dbg);  \
+    else if (mode == 0) launch_head<CC, CC, 0, false>(c, F, n, L, lut, X, cf, cdf, a_dbg);       \
+    else if (L.can_saturate) launch_head<CC, CC, 1, true>(c, F, n, L, lut, X, cf, cdf, a_dbg);   \
+    else launch_head<CC, CC, 1, false>(c, F, n, L, lut, X, cf, cdf, a_dbg);                      \
     return;                                                                  \
   }
   PCC_HEAD(8)

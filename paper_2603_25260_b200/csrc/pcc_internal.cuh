@@ -48,6 +48,8 @@ struct DHead {       // Predictor: W1 [H][C], b1, rq1; W2 [256][H] (row 255 = 0)
   // Saturation thresholds of the logit requant (exact, computed at load): z > zsat_hi
   // gives +2^24, z < zsat_lo gives -2^24, otherwise the result fits in 32 bits.
   int32_t zsat_lo, zsat_hi;
+  // false when max_i(|b2_i| + 128 sum_h |W2_ih|) is inside both thresholds
+  bool can_saturate;
 };
 struct DShallow {
   DConv a, b;

@@ -274,6 +274,15 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
       std::memcpy(b2.data(), r.take(size_t(4) * NCODE), size_t(4) * NCODE);
       hd.rql = r.rq();
       logit_saturation(hd.rql, hd.zsat_lo, hd.zsat_hi);
+      {  // |z_i| <= |b2_i| + 128 * sum_h |W2_ih| since |a_h| <= 128
+        int64_t zb = 0;
+        for (int i = 0; i < NCODE; ++i) {
+          int64_t s = std::abs(int64_t(b2[i]));
+          for (int h2 = 0; h2 < H; ++h2) s += 128 * std::abs(int64_t(W2[size_t(i) * H + h2]));
+          zb = std::max(zb, s);
+        }
+        hd.can_saturate = zb > hd.zsat_hi || -zb < hd.zsat_lo;
+      }
       hd.W2 = off_ptr<const int8_t>(st.put(W2.data(), W2.size()));
       hd.b2 = off_ptr<const int32_t>(st.put(b2.data(), b2.size() * 4));
       return hd;
