@@ -326,26 +326,26 @@ def run_ours(args, rank, world, dist):
         gpu_launches += pcc.pcc_ctx_launch_count(ln.ctx)
     gpu_launches *= K
 
-    # ---- profiled pass (CUDA events around every launch, same streams; lanes serial) ----
+    # ---- profiled pass: CUDA events around every launch of ONE codec instance holding the
+    #      whole batch (no lane overlap, so per-kernel durations and shares are not
+    #      inflated by concurrent streams) ----
     KP = max(1, min(K, 3))
-    for ln in lanes:
-        pcc.pcc_ctx_set_profile(ln.ctx, True)
+    full = Lane(0, B) if S > 1 else lanes[0]
+    pcc.pcc_ctx_set_profile(full.ctx, True)
     for _ in range(KP):
         with torch.cuda.stream(main):
             flush.zero_()
         torch.cuda.synchronize(dev)
-        for ln in lanes:
-            ln.run()
+        full.run()
         torch.cuda.synchronize(dev)
     prof = {}
-    for ln in lanes:
-        for cname in pcc.pcc_ctx_profile_categories(ln.ctx):
-            ms, nl, nb = pcc.pcc_ctx_profile_get(ln.ctx, cname)
-            d = prof.setdefault(cname, {"ms_per_step": 0.0, "launches_per_step": 0.0, "bytes_per_step": 0.0})
-            d["ms_per_step"] += ms / KP
-            d["launches_per_step"] += nl / KP
-            d["bytes_per_step"] += nb / KP
-        pcc.pcc_ctx_set_profile(ln.ctx, False)
+    for cname in pcc.pcc_ctx_profile_categories(full.ctx):
+        ms, nl, nb = pcc.pcc_ctx_profile_get(full.ctx, cname)
+        prof[cname] = {"ms_per_step": ms / KP, "launches_per_step": nl / KP, "bytes_per_step": nb / KP}
+    pcc.pcc_ctx_set_profile(full.ctx, False)
+    if full is not lanes[0]:
+        pcc.pcc_ctx_destroy(full.ctx)
+        del full
     prof_total = sum(v["ms_per_step"] for v in prof.values())
 
     # ---- e2e through the host-buffer C ABI (H2D inputs + D2H results inside), one lane
