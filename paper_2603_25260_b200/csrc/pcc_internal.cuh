@@ -37,6 +37,10 @@ struct DUp {         // Upsampling over Concat(S, onehot X): W_S [8C][C], E [255
   const int32_t* E;
   const int32_t* b;
   RQ rq;
+  // the literal Concat+Linear weight for the tensor-core kernel: [8C][C + 256] int8,
+  // columns C..C+254 = W_X (one-hot part), column C+255 = 0; q_one = the one-hot value
+  const int8_t* Wcat;
+  int32_t q_one;
 };
 struct DHead {       // Predictor: W1 [H][C], b1, rq1; W2 [256][H] (row 255 = 0), b2 [256]; logit rq
   const int8_t* W1;

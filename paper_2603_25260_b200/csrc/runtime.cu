@@ -255,12 +255,18 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
       const uint8_t* b = r.take(size_t(4) * 8 * C);
       u.rq = r.rq();
       const int32_t q_one = r.i32();
+      if (q_one < -128 || q_one > 127) throw Error{PCC_ERR_INVALID_ARG};  // an int8 activation
       std::vector<int32_t> E(size_t(NCODE) * 8 * C);  // E[v][o] = q_one * W[o][C + v] (exact)
       for (int v = 0; v < NCODE; ++v)
         for (int o = 0; o < 8 * C; ++o) E[size_t(v) * 8 * C + o] = q_one * int32_t(int8_t(W[size_t(o) * (C + NCODE) + C + v]));
+      std::vector<int8_t> Wcat(size_t(8) * C * (C + 256), 0);
+      for (int o = 0; o < 8 * C; ++o)
+        for (int i = 0; i < C + NCODE; ++i) Wcat[size_t(o) * (C + 256) + i] = int8_t(W[size_t(o) * (C + NCODE) + i]);
+      u.q_one = q_one;
       u.W = off_ptr<const int8_t>(st.put(WS.data(), WS.size()));
       u.E = off_ptr<const int32_t>(st.put(E.data(), E.size() * 4));
       u.b = off_ptr<const int32_t>(st.put(b, size_t(4) * 8 * C));
+      u.Wcat = off_ptr<const int8_t>(st.put(Wcat.data(), Wcat.size()));
       return u;
     };
     auto head = [&]() {
@@ -326,7 +332,9 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
     auto rb_head = [&](DHead& hd) {
       hd.W1 = rebase(hd.W1, base); hd.b1 = rebase(hd.b1, base); hd.W2 = rebase(hd.W2, base); hd.b2 = rebase(hd.b2, base);
     };
-    auto rb_up = [&](DUp& u) { u.W = rebase(u.W, base); u.E = rebase(u.E, base); u.b = rebase(u.b, base); };
+    auto rb_up = [&](DUp& u) {
+      u.W = rebase(u.W, base); u.E = rebase(u.E, base); u.b = rebase(u.b, base); u.Wcat = rebase(u.Wcat, base);
+    };
     for (auto& s : m->shallow) {
       s.a.W = rebase(s.a.W, base); s.a.b = rebase(s.a.b, base);
       s.b.W = rebase(s.b.W, base); s.b.b = rebase(s.b.b, base);

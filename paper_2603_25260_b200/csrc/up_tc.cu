@@ -4,11 +4,12 @@
 // Upsampling is "a linear transformation followed by a PReLU activation, performing an
 // 8x channel expansion" over Concat(S, X) (reading Q6: the one-hot half is the int32 row
 // E[X] = q_one * W_X[:, X]); Pruning "discards features of unoccupied child nodes".
-// Per tile of 128 parents: the parent rows (cp.async into the canonical K-major A tile)
-// times W_S [256 x 32] is ONE tcgen05.mma.kind::i8 (M = 128, N = 256, K = 32) into TMEM.
-// Epilogue: 4 threads per parent (TMEM lane), thread quarter q owns child blocks
-// c = 2q, 2q+1 (columns 64q..64q+63); for each occupied child c it adds the bias and
-// E[X][c], PReLU-requantises the 32 outputs and writes the child row
+// Per tile of 128 parents the A operand is the literal concatenation [S | q_one*onehot(X)]
+// (K = 32 + 256, one-hot built in smem), times the model's Concat+Linear weight
+// [256 x 288]: nine tcgen05.mma.kind::i8 (M = 128, N = 256, K = 32) into one TMEM
+// accumulator.  Epilogue: 4 threads per parent (TMEM lane), thread quarter q owns child
+// blocks c = 2q, 2q+1 (columns 64q..64q+63); for each occupied child c it adds the bias,
+// PReLU-requantises the 32 outputs and writes the child row
 // child_start[p] + rank(c) (children are contiguous and in Morton order, reading Q8).
 // Bit-exact with the dp4a kernel and the oracle's up_prune.
 #include "pcc_internal.cuh"
@@ -41,24 +42,33 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 
+// smem: B = Wcat as 9 K-slabs of 256 x 32 (72 KB), A = 9 K-slabs of 128 x 32 (36 KB):
+// slab 0 the parent rows S, slabs 1..8 the one-hot of X (q_one at column X-1).
+constexpr int KSL = 9;
+constexpr int SM_B = 0, SM_A = KSL * 8192, SM_BIAS = SM_A + KSL * 4096, SM_MBAR = SM_BIAS + 1024;
+constexpr int SM_END = SM_MBAR + 64;
+
 __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, const uint8_t* __restrict__ Xp,
                                                   const uint32_t* __restrict__ cs, uint32_t np, uint32_t nc,
-                                                  const int8_t* __restrict__ W, const int32_t* __restrict__ E,
-                                                  const int32_t* __restrict__ bias, RQ rq, int8_t* __restrict__ out) {
+                                                  const int8_t* __restrict__ Wcat, const int32_t* __restrict__ bias,
+                                                  RQ rq, int32_t q_one, int8_t* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  uint8_t* sB = sm;                 // W_S as 256 x 32 canonical (8 KB)
-  uint8_t* sA = sm + 8192;          // 128 x 32 canonical (4 KB)
-  int32_t* sbias = reinterpret_cast<int32_t*>(sm + 12288);  // 256 x int32
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + 13312);
-  uint32_t* thold = reinterpret_cast<uint32_t*>(sm + 13320);
+  uint8_t* sB = sm + SM_B;
+  uint8_t* sA = sm + SM_A;
+  int32_t* sbias = reinterpret_cast<int32_t*>(sm + SM_BIAS);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + SM_MBAR);
+  uint32_t* thold = reinterpret_cast<uint32_t*>(sm + SM_MBAR + 8);
   const int t = threadIdx.x, warp = t >> 5;
   const int r = 32 * (warp & 3) + (t & 31);  // parent of the tile (= TMEM lane)
   const int q = warp >> 2;                   // child blocks 2q, 2q+1
 
-  for (int k = t; k < 256 * 2; k += UNT) {  // W_S [256][32]: 2 x 16-byte chunks per row
-    const int o = k >> 1, h = k & 1;
-    *reinterpret_cast<uint4*>(sB + tc::kmaj_off(o, 16 * h)) = reinterpret_cast<const uint4*>(W)[k];
+  // Wcat [256][288]: 18 x 16-byte chunks per output row -> slab h/2, K half h%2
+  for (int k = t; k < 256 * 18; k += UNT) {
+    const int o = k / 18, h = k % 18;
+    *reinterpret_cast<uint4*>(sB + (h >> 1) * 8192 + tc::kmaj_off(o, 16 * (h & 1))) =
+        reinterpret_cast<const uint4*>(Wcat)[k];
   }
+  for (int k = t; k < KSL * 4096 / 16; k += UNT) reinterpret_cast<uint4*>(sA)[k] = make_uint4(0u, 0u, 0u, 0u);
   for (int k = t; k < 256; k += UNT) sbias[k] = bias[k];
   if (warp == 0) tc::tmem_alloc<256>(thold);
   if (t == 0) tc::mbar_init(mbar, 1);
@@ -68,8 +78,6 @@ __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, 
   tc::fence_after();
   const uint32_t tbase = *thold;
   const uint32_t taddr = tbase + (uint32_t(32 * (warp & 3)) << 16);
-  const uint64_t adesc = tc::sdesc(tc::smem_u32(sA));
-  const uint64_t bdesc = tc::sdesc(tc::smem_u32(sB));
   const uint32_t ntiles = (np + UT - 1) / UT;
   uint32_t phase = 0;
   if (blockIdx.x == 0 && t < 8) reinterpret_cast<uint32_t*>(out + size_t(nc) * 32)[t] = 0u;  // zero row
@@ -77,11 +85,18 @@ __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, 
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint32_t p = tile * UT + r;
     const bool valid = p < np;
-    if (t < 2 * UT) {  // A tile: parent rows, two 16-byte halves each
+    const uint32_t x = valid ? uint32_t(Xp[p]) : 0u;
+    const uint32_t c0 = valid ? cs[p] : 0u;
+    uint8_t* hot = nullptr;  // this row's one-hot byte (set by quarter 0)
+    if (t < 2 * UT) {  // slab 0: parent rows, two 16-byte halves each
       const int rr = t >> 1, h = t & 1;
       const uint32_t pp = tile * UT + rr;
       if (pp < np) cp16(sA + tc::kmaj_off(rr, 16 * h), S + size_t(pp) * 32 + 16 * h);
       else *reinterpret_cast<uint4*>(sA + tc::kmaj_off(rr, 16 * h)) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (q == 0 && x != 0u) {  // Concat(S, X): q_one at one-hot column x-1 (reading Q6)
+      hot = sA + (1 + (x - 1) / 32) * 4096 + tc::kmaj_off(r, (x - 1) % 32);
+      *hot = uint8_t(int8_t(q_one));
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     tc::fence_async_smem();
@@ -89,14 +104,16 @@ __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, 
     __syncthreads();
     tc::fence_after();
     if (t == 0) {
-      tc::mma_i8(tbase, adesc, bdesc, IDESC_UP, 0u);
+#pragma unroll
+      for (int s = 0; s < KSL; ++s)
+        tc::mma_i8(tbase, tc::sdesc(tc::smem_u32(sA + s * 4096)), tc::sdesc(tc::smem_u32(sB + s * 8192)), IDESC_UP,
+                   s > 0 ? 1u : 0u);
       tc::commit(mbar);
     }
-    const uint32_t x = valid ? uint32_t(Xp[p]) : 0u;
-    const uint32_t c0 = valid ? cs[p] : 0u;
     tc::mbar_wait(mbar, phase);
     phase ^= 1u;
     tc::fence_after();
+    if (hot) *hot = 0u;  // the MMAs have consumed the tile: restore the all-zero one-hot slabs
 #pragma unroll
     for (int cc = 0; cc < 2; ++cc) {
       const int c = 2 * q + cc;
@@ -108,16 +125,14 @@ __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, 
         tmem_ld16(taddr + uint32_t(32 * c + 16), *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
         tc::tmem_wait_ld();
         if (occ) {
-          const int4* e4 = reinterpret_cast<const int4*>(E + size_t(x - 1) * 256 + 32 * c);
           uint32_t w[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            const int4 e = e4[k];
             const int32_t* bb = sbias + 32 * c + 4 * k;
-            const uint32_t b0 = uint32_t(rq8(int32_t(v[4 * k]) + e.x + bb[0], rq)) & 0xffu;
-            const uint32_t b1 = uint32_t(rq8(int32_t(v[4 * k + 1]) + e.y + bb[1], rq)) & 0xffu;
-            const uint32_t b2 = uint32_t(rq8(int32_t(v[4 * k + 2]) + e.z + bb[2], rq)) & 0xffu;
-            const uint32_t b3 = uint32_t(rq8(int32_t(v[4 * k + 3]) + e.w + bb[3], rq)) & 0xffu;
+            const uint32_t b0 = uint32_t(rq8(int32_t(v[4 * k]) + bb[0], rq)) & 0xffu;
+            const uint32_t b1 = uint32_t(rq8(int32_t(v[4 * k + 1]) + bb[1], rq)) & 0xffu;
+            const uint32_t b2 = uint32_t(rq8(int32_t(v[4 * k + 2]) + bb[2], rq)) & 0xffu;
+            const uint32_t b3 = uint32_t(rq8(int32_t(v[4 * k + 3]) + bb[3], rq)) & 0xffu;
             w[k] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
           }
           const uint32_t row = c0 + __popc(x & ((1u << c) - 1u));
@@ -139,7 +154,7 @@ __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, 
 
 void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* cs_p, uint32_t np, uint32_t nc,
                  const DUp& L, int8_t* out) {
-  constexpr int smem = 80 * 1024;  // caps residency at 2 CTAs/SM (TMEM: 2 x 256 cols)
+  constexpr int smem = SM_END;  // ~109 KB: at most 2 CTAs/SM (also the TMEM limit, 2 x 256 cols)
   static bool attr = false;
   if (!attr) {
     PCC_CUDA(cudaFuncSetAttribute(k_up_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -148,7 +163,7 @@ void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* 
   const uint32_t ntiles = (np + UT - 1) / UT;
   const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 2u));
   Prof p(c, "up", size_t(nc) * 32 + size_t(np) * (32 + 1 + 4));
-  k_up_tc<<<grid, UNT, smem, c->stream>>>(S, Xp, cs_p, np, nc, L.W, L.E, L.b, L.rq, out);
+  k_up_tc<<<grid, UNT, smem, c->stream>>>(S, Xp, cs_p, np, nc, L.Wcat, L.b, L.rq, L.q_one, out);
   launched(c);
 }
 
