@@ -15,6 +15,7 @@
 // of the row's 32 accumulators, bias, skip, PReLU-requant, 32-byte store.
 // Bit-exact with the dp4a kernel and the oracle (int32 addition is associative, O6).
 #include "pcc_internal.cuh"
+#include "rq.cuh"
 #include "tc.cuh"
 
 namespace pcc {
@@ -44,12 +45,6 @@ constexpr int NSTAGE = 3;  // barrier slots: 0, 1 = A buffers, NSTAGE = tile don
 // kernel offsets gathered per barrier (2 A buffers of GROUP x SLABS x 4 KB; 2 CTAs/SM)
 __host__ __device__ constexpr int group_of(int slabs) { return slabs == 1 ? 7 : 3; }
 constexpr uint32_t IDESC32 = tc::idesc_i8(128, 32);
-
-__device__ __forceinline__ int32_t rq8(int32_t acc, RQ q) {
-  int64_t v = int64_t(acc) * int64_t(acc >= 0 ? q.mp : q.mn);
-  if (q.r > 0) v = (v + (int64_t(1) << (q.r - 1))) >> q.r;
-  return int32_t(v < -128 ? -128 : (v > 127 ? 127 : v));
-}
 
 __device__ __forceinline__ void cp16(void* s, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(s)), "l"(g));

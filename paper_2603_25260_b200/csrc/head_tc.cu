@@ -15,6 +15,7 @@
 //      written with coalesced stores).
 // Bit-exact with the oracle's cdf_quantize / head_logits (integer arithmetic only).
 #include "pcc_internal.cuh"
+#include "rq.cuh"
 #include "tc.cuh"
 
 namespace pcc {
@@ -24,12 +25,6 @@ namespace {
 constexpr int TILE = 128;
 constexpr uint32_t IDESC = tc::idesc_i8(128, 256);
 constexpr int STG = 264;  // staged cdf row stride in u16 (528 B: 16-B aligned, STS.128/LDS.128 conflict-free)
-
-__device__ __forceinline__ int32_t rq8(int32_t acc, RQ q) {
-  int64_t v = int64_t(acc) * int64_t(acc >= 0 ? q.mp : q.mn);
-  if (q.r > 0) v = (v + (int64_t(1) << (q.r - 1))) >> q.r;
-  return int32_t(v < -128 ? -128 : (v > 127 ? 127 : v));
-}
 
 __device__ __forceinline__ int32_t lq8(int32_t z, RQ q) {  // Q8 logit, clamp +-2^24
   int64_t v = int64_t(z) * int64_t(q.mp);

@@ -5,16 +5,11 @@
 // fixed-point requant q = clip((acc*m + 2^(r-1)) >> r) with PReLU fused as a sign-
 // selected multiplier (Eq.14; readings Q15, Q18).
 #include "pcc_internal.cuh"
+#include "rq.cuh"
 
 namespace pcc {
 
 namespace {
-
-__device__ __forceinline__ int32_t rq8(int32_t acc, RQ q) {
-  int64_t v = int64_t(acc) * int64_t(acc >= 0 ? q.mp : q.mn);
-  if (q.r > 0) v = (v + (int64_t(1) << (q.r - 1))) >> q.r;
-  return int32_t(v < -128 ? -128 : (v > 127 ? 127 : v));
-}
 
 __device__ __forceinline__ uint32_t pack4(int32_t a, int32_t b, int32_t c, int32_t d) {
   return (uint32_t(a) & 0xffu) | (uint32_t(b) & 0xffu) << 8 | (uint32_t(c) & 0xffu) << 16 | (uint32_t(d) & 0xffu) << 24;

@@ -25,6 +25,9 @@ enum : uint32_t {
 
 struct RQ {  // fixed-point requant, Eq.14; m_neg != m_pos = fused PReLU (reading Q18)
   int32_t mp, mn, r;
+  // precomputed by rq_prepare (rq.cuh): the one-multiply exact form when fast != 0
+  int32_t fast;
+  uint32_t Mp, Mn, Ap, An;
 };
 
 struct DConv {       // K3S1 conv: W [27][cout][cin], b [cout]
@@ -37,10 +40,8 @@ struct DUp {         // Upsampling over Concat(S, onehot X): W_S [8C][C], E [255
   const int32_t* E;
   const int32_t* b;
   RQ rq;
-  // the literal Concat+Linear weight for the tensor-core kernel: [8C][C + 256] int8,
-  // columns C..C+254 = W_X (one-hot part), column C+255 = 0; q_one = the one-hot value
-  const int8_t* Wcat;
-  int32_t q_one;
+  // Eb [255][8C] = E + b: the one-hot half and the bias in one int32 row (exact sum)
+  const int32_t* Eb;
 };
 struct DHead {       // Predictor: W1 [H][C], b1, rq1; W2 [256][H] (row 255 = 0), b2 [256]; logit rq
   const int8_t* W1;

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "pcc_internal.cuh"
+#include "rq.cuh"
 
 using namespace pcc;
 
@@ -147,6 +148,7 @@ struct Rd {
     t.r = i32();
     // reading O5: m in [0, 2^31), r in [0, 62] (m >= 0 keeps every requant monotone)
     if (t.r < 0 || t.r > 62 || t.mp < 0 || t.mn < 0) throw Error{PCC_ERR_INVALID_ARG};
+    rq_prepare(t);
     return t;
   }
 };
@@ -259,14 +261,17 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
       std::vector<int32_t> E(size_t(NCODE) * 8 * C);  // E[v][o] = q_one * W[o][C + v] (exact)
       for (int v = 0; v < NCODE; ++v)
         for (int o = 0; o < 8 * C; ++o) E[size_t(v) * 8 * C + o] = q_one * int32_t(int8_t(W[size_t(o) * (C + NCODE) + C + v]));
-      std::vector<int8_t> Wcat(size_t(8) * C * (C + 256), 0);
-      for (int o = 0; o < 8 * C; ++o)
-        for (int i = 0; i < C + NCODE; ++i) Wcat[size_t(o) * (C + 256) + i] = int8_t(W[size_t(o) * (C + NCODE) + i]);
-      u.q_one = q_one;
+      std::vector<int32_t> Eb(E);
+      for (int v = 0; v < NCODE; ++v)
+        for (int o = 0; o < 8 * C; ++o) {
+          int32_t bo;
+          std::memcpy(&bo, b + size_t(4) * o, 4);
+          Eb[size_t(v) * 8 * C + o] += bo;
+        }
       u.W = off_ptr<const int8_t>(st.put(WS.data(), WS.size()));
       u.E = off_ptr<const int32_t>(st.put(E.data(), E.size() * 4));
       u.b = off_ptr<const int32_t>(st.put(b, size_t(4) * 8 * C));
-      u.Wcat = off_ptr<const int8_t>(st.put(Wcat.data(), Wcat.size()));
+      u.Eb = off_ptr<const int32_t>(st.put(Eb.data(), Eb.size() * 4));
       return u;
     };
     auto head = [&]() {
@@ -333,7 +338,7 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
       hd.W1 = rebase(hd.W1, base); hd.b1 = rebase(hd.b1, base); hd.W2 = rebase(hd.W2, base); hd.b2 = rebase(hd.b2, base);
     };
     auto rb_up = [&](DUp& u) {
-      u.W = rebase(u.W, base); u.E = rebase(u.E, base); u.b = rebase(u.b, base); u.Wcat = rebase(u.Wcat, base);
+      u.W = rebase(u.W, base); u.E = rebase(u.E, base); u.b = rebase(u.b, base); u.Eb = rebase(u.Eb, base);
     };
     for (auto& s : m->shallow) {
       s.a.W = rebase(s.a.W, base); s.a.b = rebase(s.a.b, base);

@@ -4,15 +4,17 @@
 // Upsampling is "a linear transformation followed by a PReLU activation, performing an
 // 8x channel expansion" over Concat(S, X) (reading Q6: the one-hot half is the int32 row
 // E[X] = q_one * W_X[:, X]); Pruning "discards features of unoccupied child nodes".
-// Per tile of 128 parents the A operand is the literal concatenation [S | q_one*onehot(X)]
-// (K = 32 + 256, one-hot built in smem), times the model's Concat+Linear weight
-// [256 x 288]: nine tcgen05.mma.kind::i8 (M = 128, N = 256, K = 32) into one TMEM
-// accumulator.  Epilogue: 4 threads per parent (TMEM lane), thread quarter q owns child
-// blocks c = 2q, 2q+1 (columns 64q..64q+63); for each occupied child c it adds the bias,
-// PReLU-requantises the 32 outputs and writes the child row
-// child_start[p] + rank(c) (children are contiguous and in Morton order, reading Q8).
-// Bit-exact with the dp4a kernel and the oracle's up_prune.
+// Transposed product on tcgen05.mma.kind::i8: D[o][p] = W_S[o] . S[p] with the 256 output
+// channels as M (two M = 128 halves, A = W_S staged once per CTA) and a tile of 128
+// parents as N (B = the parent rows, cp.async, double-buffered): TMEM lane = channel,
+// column = parent.  A warp of lane quarter q reads channel block c of 16 parents per
+// tcgen05.ld, so the occupancy test "does parent p have child c" is uniform across the
+// warp: no lane idles on pruned children.  The one-hot half plus the bias is one int32
+// row Eb[X][o] = q_one*W_X[o][X] + b[o] (exact; reading Q6), a coalesced 128-B load per
+// kept child; then the fast exact requant (rq.cuh) and one byte per lane of the child
+// row child_start[p] + rank(c) (children contiguous, Morton order, reading Q8).
 #include "pcc_internal.cuh"
+#include "rq.cuh"
 #include "tc.cuh"
 
 namespace pcc {
@@ -21,13 +23,7 @@ namespace {
 
 constexpr int UT = 128;  // parents per tile
 constexpr int UNT = 512; // threads per CTA (4 per parent)
-constexpr uint32_t IDESC_UP = tc::idesc_i8(128, 256);
-
-__device__ __forceinline__ int32_t rq8(int32_t acc, RQ q) {
-  int64_t v = int64_t(acc) * int64_t(acc >= 0 ? q.mp : q.mn);
-  if (q.r > 0) v = (v + (int64_t(1) << (q.r - 1))) >> q.r;
-  return int32_t(v < -128 ? -128 : (v > 127 ? 127 : v));
-}
+constexpr uint32_t IDESC_UP = tc::idesc_i8(128, UT);
 
 __device__ __forceinline__ void cp16(void* s, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(s)), "l"(g));
@@ -42,108 +38,100 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 
-// smem: B = Wcat as 9 K-slabs of 256 x 32 (72 KB), A = 9 K-slabs of 128 x 32 (36 KB):
-// slab 0 the parent rows S, slabs 1..8 the one-hot of X (q_one at column X-1).
-constexpr int KSL = 9;
-constexpr int SM_B = 0, SM_A = KSL * 8192, SM_BIAS = SM_A + KSL * 4096, SM_MBAR = SM_BIAS + 1024;
+// smem: A = W_S as two [128 x 32] canonical K-major halves (8 KB); per buffer: the parent
+// tile [128 x 32] (4 KB), its codes and child starts.
+constexpr int SM_A = 0, SM_S = 8192, SM_X = SM_S + 2 * 4096, SM_CS = SM_X + 2 * UT, SM_MBAR = SM_CS + 2 * UT * 4;
 constexpr int SM_END = SM_MBAR + 64;
 
 __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, const uint8_t* __restrict__ Xp,
                                                   const uint32_t* __restrict__ cs, uint32_t np, uint32_t nc,
-                                                  const int8_t* __restrict__ Wcat, const int32_t* __restrict__ bias,
-                                                  RQ rq, int32_t q_one, int8_t* __restrict__ out) {
+                                                  const int8_t* __restrict__ WS, const int32_t* __restrict__ Eb,
+                                                  RQ rq, int8_t* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  uint8_t* sB = sm + SM_B;
   uint8_t* sA = sm + SM_A;
-  int32_t* sbias = reinterpret_cast<int32_t*>(sm + SM_BIAS);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + SM_MBAR);
   uint32_t* thold = reinterpret_cast<uint32_t*>(sm + SM_MBAR + 8);
-  const int t = threadIdx.x, warp = t >> 5;
-  const int r = 32 * (warp & 3) + (t & 31);  // parent of the tile (= TMEM lane)
-  const int q = warp >> 2;                   // child blocks 2q, 2q+1
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int qd = warp & 3;          // TMEM lane quarter: channels 32qd.. of a half
+  const int hv = (warp >> 2) & 1;   // channel half -> child block c = 4hv + qd
+  const int c = 4 * hv + qd;
+  const int pr = warp >> 3;         // parents 64pr .. 64pr+63 of the tile
+  const uint32_t below = (1u << c) - 1u;
 
-  // Wcat [256][288]: 18 x 16-byte chunks per output row -> slab h/2, K half h%2
-  for (int k = t; k < 256 * 18; k += UNT) {
-    const int o = k / 18, h = k % 18;
-    *reinterpret_cast<uint4*>(sB + (h >> 1) * 8192 + tc::kmaj_off(o, 16 * (h & 1))) =
-        reinterpret_cast<const uint4*>(Wcat)[k];
+  // W_S [256][32]: row o -> half o/128, row o%128 (two 16-byte chunks per row)
+  for (int k = t; k < 512; k += UNT) {
+    const int o = k >> 1, h = k & 1;
+    *reinterpret_cast<uint4*>(sA + (o >> 7) * 4096 + tc::kmaj_off(o & 127, 16 * h)) =
+        reinterpret_cast<const uint4*>(WS)[k];
   }
-  for (int k = t; k < KSL * 4096 / 16; k += UNT) reinterpret_cast<uint4*>(sA)[k] = make_uint4(0u, 0u, 0u, 0u);
-  for (int k = t; k < 256; k += UNT) sbias[k] = bias[k];
   if (warp == 0) tc::tmem_alloc<256>(thold);
   if (t == 0) tc::mbar_init(mbar, 1);
+  const uint32_t ntiles = (np + UT - 1) / UT;
+  if (blockIdx.x == 0 && t < 8) reinterpret_cast<uint32_t*>(out + size_t(nc) * 32)[t] = 0u;  // zero row
+
+  // stage tile `tile` into buffer `b`: parent rows by cp.async, codes / child starts by threads 256..383
+  auto stage = [&](uint32_t tile, int b) {
+    uint8_t* sS = sm + SM_S + b * 4096;
+    if (t < 2 * UT) {
+      const int rr = t >> 1, h = t & 1;
+      const uint32_t pp = tile * UT + rr;
+      if (pp < np) cp16(sS + tc::kmaj_off(rr, 16 * h), S + size_t(pp) * 32 + 16 * h);
+      else *reinterpret_cast<uint4*>(sS + tc::kmaj_off(rr, 16 * h)) = make_uint4(0u, 0u, 0u, 0u);
+    } else if (t < 3 * UT) {
+      const int rr = t - 2 * UT;
+      const uint32_t pp = tile * UT + rr;
+      sm[SM_X + b * UT + rr] = pp < np ? Xp[pp] : uint8_t(0);
+      reinterpret_cast<uint32_t*>(sm + SM_CS)[b * UT + rr] = pp < np ? cs[pp] : 0u;
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if (blockIdx.x < ntiles) stage(blockIdx.x, 0);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   tc::fence_async_smem();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = *thold;
-  const uint32_t taddr = tbase + (uint32_t(32 * (warp & 3)) << 16);
-  const uint32_t ntiles = (np + UT - 1) / UT;
   uint32_t phase = 0;
-  if (blockIdx.x == 0 && t < 8) reinterpret_cast<uint32_t*>(out + size_t(nc) * 32)[t] = 0u;  // zero row
+  int buf = 0;
 
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t p = tile * UT + r;
-    const bool valid = p < np;
-    const uint32_t x = valid ? uint32_t(Xp[p]) : 0u;
-    const uint32_t c0 = valid ? cs[p] : 0u;
-    uint8_t* hot = nullptr;  // this row's one-hot byte (set by quarter 0)
-    if (t < 2 * UT) {  // slab 0: parent rows, two 16-byte halves each
-      const int rr = t >> 1, h = t & 1;
-      const uint32_t pp = tile * UT + rr;
-      if (pp < np) cp16(sA + tc::kmaj_off(rr, 16 * h), S + size_t(pp) * 32 + 16 * h);
-      else *reinterpret_cast<uint4*>(sA + tc::kmaj_off(rr, 16 * h)) = make_uint4(0u, 0u, 0u, 0u);
-    }
-    if (q == 0 && x != 0u) {  // Concat(S, X): q_one at one-hot column x-1 (reading Q6)
-      hot = sA + (1 + (x - 1) / 32) * 4096 + tc::kmaj_off(r, (x - 1) % 32);
-      *hot = uint8_t(int8_t(q_one));
-    }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-    tc::fence_async_smem();
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
     if (t == 0) {
-#pragma unroll
-      for (int s = 0; s < KSL; ++s)
-        tc::mma_i8(tbase, tc::sdesc(tc::smem_u32(sA + s * 4096)), tc::sdesc(tc::smem_u32(sB + s * 8192)), IDESC_UP,
-                   s > 0 ? 1u : 0u);
+      const uint64_t bdesc = tc::sdesc(tc::smem_u32(sm + SM_S + buf * 4096));
+      tc::mma_i8(tbase, tc::sdesc(tc::smem_u32(sA)), bdesc, IDESC_UP, 0u);
+      tc::mma_i8(tbase + 128, tc::sdesc(tc::smem_u32(sA + 4096)), bdesc, IDESC_UP, 0u);
       tc::commit(mbar);
     }
+    if (tile + gridDim.x < ntiles) stage(tile + gridDim.x, buf ^ 1);  // overlaps the MMA + epilogue
     tc::mbar_wait(mbar, phase);
     phase ^= 1u;
     tc::fence_after();
-    if (hot) *hot = 0u;  // the MMAs have consumed the tile: restore the all-zero one-hot slabs
+    const uint8_t* sX = sm + SM_X + buf * UT;
+    const uint32_t* sCS = reinterpret_cast<const uint32_t*>(sm + SM_CS) + buf * UT;
+#pragma unroll 1
+    for (int j0 = 64 * pr; j0 < 64 * pr + 64; j0 += 16) {
+      uint32_t v[16];
+      tmem_ld16(tbase + (uint32_t(32 * qd) << 16) + uint32_t(128 * hv + j0), v);
+      uint32_t xs[16];
+      int32_t e[16];
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-      const int c = 2 * q + cc;
-      const bool occ = (x >> c) & 1u;
-      // warp-collective TMEM loads: issue only if some parent of this warp has child c
-      if (__any_sync(0xffffffffu, occ)) {
-        uint32_t v[32];
-        tmem_ld16(taddr + uint32_t(32 * c), *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
-        tmem_ld16(taddr + uint32_t(32 * c + 16), *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
-        tc::tmem_wait_ld();
-        if (occ) {
-          uint32_t w[8];
+      for (int i = 0; i < 16; ++i) {
+        xs[i] = sX[j0 + i];
+        e[i] = ((xs[i] >> c) & 1u) ? __ldg(Eb + size_t(xs[i] - 1) * 256 + 32 * c + lane) : 0;
+      }
+      tc::tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int32_t* bb = sbias + 32 * c + 4 * k;
-            const uint32_t b0 = uint32_t(rq8(int32_t(v[4 * k]) + bb[0], rq)) & 0xffu;
-            const uint32_t b1 = uint32_t(rq8(int32_t(v[4 * k + 1]) + bb[1], rq)) & 0xffu;
-            const uint32_t b2 = uint32_t(rq8(int32_t(v[4 * k + 2]) + bb[2], rq)) & 0xffu;
-            const uint32_t b3 = uint32_t(rq8(int32_t(v[4 * k + 3]) + bb[3], rq)) & 0xffu;
-            w[k] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
-          }
-          const uint32_t row = c0 + __popc(x & ((1u << c) - 1u));
-          uint4* o4 = reinterpret_cast<uint4*>(out + size_t(row) * 32);
-          o4[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          o4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      for (int i = 0; i < 16; ++i) {
+        if ((xs[i] >> c) & 1u) {  // warp-uniform
+          const uint32_t row = sCS[j0 + i] + __popc(xs[i] & below);
+          out[size_t(row) * 32 + lane] = int8_t(rq8(int32_t(v[i]) + e[i], rq));
         }
       }
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    tc::fence_async_smem();
     tc::fence_before();
-    __syncthreads();  // TMEM and the A tile are reused by the next tile
+    __syncthreads();  // TMEM and the staged tile are reused by the next tile
     tc::fence_after();
   }
   __syncthreads();
@@ -154,7 +142,7 @@ __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, 
 
 void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* cs_p, uint32_t np, uint32_t nc,
                  const DUp& L, int8_t* out) {
-  constexpr int smem = SM_END;  // ~109 KB: at most 2 CTAs/SM (also the TMEM limit, 2 x 256 cols)
+  constexpr int smem = SM_END;  // ~18 KB; residency is set by TMEM (2 x 256 columns per SM)
   static bool attr = false;
   if (!attr) {
     PCC_CUDA(cudaFuncSetAttribute(k_up_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -163,7 +151,7 @@ void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* 
   const uint32_t ntiles = (np + UT - 1) / UT;
   const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 2u));
   Prof p(c, "up", size_t(nc) * 32 + size_t(np) * (32 + 1 + 4));
-  k_up_tc<<<grid, UNT, smem, c->stream>>>(S, Xp, cs_p, np, nc, L.Wcat, L.b, L.rq, L.q_one, out);
+  k_up_tc<<<grid, UNT, smem, c->stream>>>(S, Xp, cs_p, np, nc, L.W, L.Eb, L.rq, out);
   launched(c);
 }
 
