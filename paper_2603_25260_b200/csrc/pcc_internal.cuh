@@ -40,8 +40,10 @@ struct DUp {         // Upsampling over Concat(S, onehot X): W_S [8C][C], E [255
   const int32_t* E;
   const int32_t* b;
   RQ rq;
-  // Eb [255][8C] = E + b: the one-hot half and the bias in one int32 row (exact sum)
-  const int32_t* Eb;
+  // WXt [255][8C] int8 = W_X transposed (row v = the weights of one-hot column v) and the
+  // one-hot value q_one, for the tensor-core kernel: E[v][o] = q_one * WXt[v][o]
+  const int8_t* WXt;
+  int32_t q_one;
 };
 struct DHead {       // Predictor: W1 [H][C], b1, rq1; W2 [256][H] (row 255 = 0), b2 [256]; logit rq
   const int8_t* W1;

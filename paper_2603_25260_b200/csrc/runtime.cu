@@ -261,17 +261,14 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
       std::vector<int32_t> E(size_t(NCODE) * 8 * C);  // E[v][o] = q_one * W[o][C + v] (exact)
       for (int v = 0; v < NCODE; ++v)
         for (int o = 0; o < 8 * C; ++o) E[size_t(v) * 8 * C + o] = q_one * int32_t(int8_t(W[size_t(o) * (C + NCODE) + C + v]));
-      std::vector<int32_t> Eb(E);
+      std::vector<int8_t> WXt(size_t(NCODE) * 8 * C);
       for (int v = 0; v < NCODE; ++v)
-        for (int o = 0; o < 8 * C; ++o) {
-          int32_t bo;
-          std::memcpy(&bo, b + size_t(4) * o, 4);
-          Eb[size_t(v) * 8 * C + o] += bo;
-        }
+        for (int o = 0; o < 8 * C; ++o) WXt[size_t(v) * 8 * C + o] = int8_t(W[size_t(o) * (C + NCODE) + C + v]);
+      u.q_one = q_one;
       u.W = off_ptr<const int8_t>(st.put(WS.data(), WS.size()));
       u.E = off_ptr<const int32_t>(st.put(E.data(), E.size() * 4));
       u.b = off_ptr<const int32_t>(st.put(b, size_t(4) * 8 * C));
-      u.Eb = off_ptr<const int32_t>(st.put(Eb.data(), Eb.size() * 4));
+      u.WXt = off_ptr<const int8_t>(st.put(WXt.data(), WXt.size()));
       return u;
     };
     auto head = [&]() {
@@ -338,7 +335,7 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
       hd.W1 = rebase(hd.W1, base); hd.b1 = rebase(hd.b1, base); hd.W2 = rebase(hd.W2, base); hd.b2 = rebase(hd.b2, base);
     };
     auto rb_up = [&](DUp& u) {
-      u.W = rebase(u.W, base); u.E = rebase(u.E, base); u.b = rebase(u.b, base); u.Eb = rebase(u.Eb, base);
+      u.W = rebase(u.W, base); u.E = rebase(u.E, base); u.b = rebase(u.b, base); u.WXt = rebase(u.WXt, base);
     };
     for (auto& s : m->shallow) {
       s.a.W = rebase(s.a.W, base); s.a.b = rebase(s.a.b, base);

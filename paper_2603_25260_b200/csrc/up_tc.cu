@@ -9,10 +9,12 @@
 // parents as N (B = the parent rows, cp.async, double-buffered): TMEM lane = channel,
 // column = parent.  A warp of lane quarter q reads channel block c of 16 parents per
 // tcgen05.ld, so the occupancy test "does parent p have child c" is uniform across the
-// warp: no lane idles on pruned children.  The one-hot half plus the bias is one int32
-// row Eb[X][o] = q_one*W_X[o][X] + b[o] (exact; reading Q6), a coalesced 128-B load per
-// kept child; then the fast exact requant (rq.cuh) and one byte per lane of the child
-// row child_start[p] + rank(c) (children contiguous, Morton order, reading Q8).
+// warp, and a warp ballot turns it into a mask that the warp walks: no lane idles on a
+// pruned child and a pruned child costs one uniform branch.  The one-hot half is
+// q_one * W_X[o][X] (reading Q6) read from a transposed copy of W_X held in smem (65 KB,
+// one conflict-free 32-byte row per kept child), the bias is a per-lane register; then
+// the fast exact requant (rq.cuh) and one byte per lane of the child row
+// child_start[p] + rank(c) (children contiguous, Morton order, reading Q8).
 #include "pcc_internal.cuh"
 #include "rq.cuh"
 #include "tc.cuh"
@@ -39,14 +41,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 
 // smem: A = W_S as two [128 x 32] canonical K-major halves (8 KB); per buffer: the parent
-// tile [128 x 32] (4 KB), its codes and child starts.
-constexpr int SM_A = 0, SM_S = 8192, SM_X = SM_S + 2 * 4096, SM_CS = SM_X + 2 * UT, SM_MBAR = SM_CS + 2 * UT * 4;
+// tile [128 x 32] (4 KB), its codes and child starts; W_X transposed [255][256] int8.
+constexpr int SM_A = 0, SM_S = 8192, SM_X = SM_S + 2 * 4096, SM_CS = SM_X + 2 * UT, SM_WX = SM_CS + 2 * UT * 4;
+constexpr int SM_MBAR = SM_WX + NCODE * 256;
 constexpr int SM_END = SM_MBAR + 64;
 
 __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, const uint8_t* __restrict__ Xp,
                                                   const uint32_t* __restrict__ cs, uint32_t np, uint32_t nc,
-                                                  const int8_t* __restrict__ WS, const int32_t* __restrict__ Eb,
-                                                  RQ rq, int8_t* __restrict__ out) {
+                                                  const int8_t* __restrict__ WS, const int8_t* __restrict__ WXt,
+                                                  const int32_t* __restrict__ bias, int32_t q_one, RQ rq,
+                                                  int8_t* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* sA = sm + SM_A;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + SM_MBAR);
@@ -64,6 +68,10 @@ __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, 
     *reinterpret_cast<uint4*>(sA + (o >> 7) * 4096 + tc::kmaj_off(o & 127, 16 * h)) =
         reinterpret_cast<const uint4*>(WS)[k];
   }
+  for (int k = t; k < NCODE * 256 / 16; k += UNT)
+    reinterpret_cast<uint4*>(sm + SM_WX)[k] = reinterpret_cast<const uint4*>(WXt)[k];
+  const int8_t* sWX = reinterpret_cast<const int8_t*>(sm + SM_WX) + 32 * c + lane - 256;  // row X-1
+  const int32_t bias_r = bias[32 * c + lane];
   if (warp == 0) tc::tmem_alloc<256>(thold);
   if (t == 0) tc::mbar_init(mbar, 1);
   const uint32_t ntiles = (np + UT - 1) / UT;
@@ -112,19 +120,20 @@ __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, 
     for (int j0 = 64 * pr; j0 < 64 * pr + 64; j0 += 16) {
       uint32_t v[16];
       tmem_ld16(tbase + (uint32_t(32 * qd) << 16) + uint32_t(128 * hv + j0), v);
-      uint32_t xs[16];
-      int32_t e[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        xs[i] = sX[j0 + i];
-        e[i] = ((xs[i] >> c) & 1u) ? __ldg(Eb + size_t(xs[i] - 1) * 256 + 32 * c + lane) : 0;
+      uint32_t xl = 0u, cl = 0u;
+      if (lane < 16) {
+        xl = sX[j0 + lane];
+        cl = sCS[j0 + lane];
       }
+      const uint32_t m = __ballot_sync(0xffffffffu, (xl >> c) & 1u);  // parents with child c
       tc::tmem_wait_ld();
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        if ((xs[i] >> c) & 1u) {  // warp-uniform
-          const uint32_t row = sCS[j0 + i] + __popc(xs[i] & below);
-          out[size_t(row) * 32 + lane] = int8_t(rq8(int32_t(v[i]) + e[i], rq));
+        if ((m >> i) & 1u) {  // warp-uniform
+          const uint32_t x = __shfl_sync(0xffffffffu, xl, i);
+          const uint32_t row = __shfl_sync(0xffffffffu, cl, i) + __popc(x & below);
+          const int32_t e = q_one * int32_t(sWX[x * 256]) + bias_r;
+          out[size_t(row) * 32 + lane] = int8_t(rq8(int32_t(v[i]) + e, rq));
         }
       }
     }
@@ -142,7 +151,7 @@ __global__ void __launch_bounds__(UNT, 2) k_up_tc(const int8_t* __restrict__ S, 
 
 void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* cs_p, uint32_t np, uint32_t nc,
                  const DUp& L, int8_t* out) {
-  constexpr int smem = SM_END;  // ~18 KB; residency is set by TMEM (2 x 256 columns per SM)
+  constexpr int smem = SM_END;  // ~83 KB: 2 CTAs/SM (also the TMEM limit, 2 x 256 columns)
   static bool attr = false;
   if (!attr) {
     PCC_CUDA(cudaFuncSetAttribute(k_up_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -151,7 +160,7 @@ void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* 
   const uint32_t ntiles = (np + UT - 1) / UT;
   const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 2u));
   Prof p(c, "up", size_t(nc) * 32 + size_t(np) * (32 + 1 + 4));
-  k_up_tc<<<grid, UNT, smem, c->stream>>>(S, Xp, cs_p, np, nc, L.W, L.Eb, L.rq, out);
+  k_up_tc<<<grid, UNT, smem, c->stream>>>(S, Xp, cs_p, np, nc, L.W, L.WXt, L.b, L.q_one, L.rq, out);
   launched(c);
 }
 
