@@ -25,9 +25,11 @@ enum : uint32_t {
 
 struct RQ {  // fixed-point requant, Eq.14; m_neg != m_pos = fused PReLU (reading Q18)
   int32_t mp, mn, r;
-  // precomputed by rq_prepare (rq.cuh): the one-multiply exact form when fast != 0
-  int32_t fast;
+  // precomputed by rq_prepare (rq.cuh): the one-multiply exact forms
+  int32_t fast;       // |x| form valid (Mp, Mn, Ap, An)
   uint32_t Mp, Mn, Ap, An;
+  int32_t fast_s;     // signed form valid (Sp, Sn)
+  int32_t Sp, Sn;
 };
 
 struct DConv {       // K3S1 conv: W [27][cout][cin], b [cout]
@@ -201,8 +203,8 @@ void gemm_i8_test(pcc_ctx c, const int8_t* dA, const int8_t* dB, int N, int32_t*
 
 // ---- up_tc.cu (parents x W_S on tcgen05, pruned epilogue; C = 32) ----
 // S: parent rows (np), Xp / cs_p: parent codes / child starts, nc: child rows (out has nc+1)
-void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* cs_p, uint32_t np, uint32_t nc,
-                 const DUp& L, int8_t* out);
+void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* par_c, const uint64_t* key_c,
+                 uint32_t nc, const DUp& L, int8_t* out);
 
 // ---- conv_tc.cu (gather -> tcgen05 kind::i8 per kernel offset; C = 32) ----
 void conv3_tc(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,

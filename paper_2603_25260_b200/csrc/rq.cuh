@@ -10,21 +10,44 @@
 //   x <  0:  rq(x) = -hi32(y * M + 2^31 - 2^(32-r))      (floor of a negative = -ceil)
 // one IMAD.WIDE.U32 instead of the 64-bit multiply/add/shift sequence; y*M + A < 2^63
 // so nothing overflows and the result is bit-identical to the generic form.
+// Signed form (RQ::fast_s, when additionally m_pos, m_neg < 2^(r-1), so M < 2^31 fits a
+// signed 32-bit operand): rq(x) = clip( (int64(x) * M + 2^31) >> 32 ) for either sign
+// (the arithmetic shift is the floor), |x * M| < 2^62: one IMAD.WIDE, no sign fix-up.
 #pragma once
 #include "pcc_internal.cuh"
 
 namespace pcc {
 
 __host__ __device__ inline void rq_prepare(RQ& q) {
-  q.fast = 0;
+  q.fast = q.fast_s = 0;
   q.Mp = q.Mn = q.Ap = q.An = 0;
+  q.Sp = q.Sn = 0;
   if (q.r >= 1 && q.r <= 32 && (int64_t(q.mp) >> q.r) == 0 && (int64_t(q.mn) >> q.r) == 0) {
     q.fast = 1;
     q.Mp = uint32_t(uint64_t(q.mp) << (32 - q.r));
     q.Mn = uint32_t(uint64_t(q.mn) << (32 - q.r));
     q.Ap = 0x80000000u;
     q.An = 0x80000000u - uint32_t(uint64_t(1) << (32 - q.r));
+    if ((int64_t(q.mp) >> (q.r - 1)) == 0 && (int64_t(q.mn) >> (q.r - 1)) == 0) {
+      q.fast_s = 1;
+      q.Sp = int32_t(q.Mp);
+      q.Sn = int32_t(q.Mn);
+    }
   }
+}
+
+// signed form, unclamped (callers saturate, e.g. with cvt.pack.sat): valid iff q.fast_s
+__device__ __forceinline__ int32_t rq_s(int32_t x, const RQ& q) {
+  const int64_t p = int64_t(x) * int64_t(x < 0 ? q.Sn : q.Sp) + (int64_t(1) << 31);
+  return int32_t(p >> 32);
+}
+
+// four int32 -> four saturated int8 packed little-endian (a lowest)
+__device__ __forceinline__ uint32_t pack_sat4(int32_t a, int32_t b, int32_t c, int32_t d) {
+  uint32_t hi, out;
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(d), "r"(c));
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(out) : "r"(b), "r"(a), "r"(hi));
+  return out;
 }
 
 __device__ __forceinline__ int32_t rq8_generic(int32_t x, const RQ& q) {

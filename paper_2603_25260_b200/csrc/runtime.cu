@@ -410,7 +410,7 @@ struct Net {
       return e && std::string(e) == "tc";
     }();
     if (C == 32 && tcv)
-      up_prune_tc(c, S, X(k), cs() + o.nb[k], o.N[k], o.N[k + 1], L, dst);
+      up_prune_tc(c, S, X(k), par() + o.nb[k + 1], key() + o.nb[k + 1], o.N[k + 1], L, dst);
     else
       up_prune(c, S, X(k), par() + o.nb[k + 1], key() + o.nb[k + 1], o.N[k + 1], C, L, dst);
   }
