@@ -401,15 +401,15 @@ struct Net {
 
   void dbgF(const std::string& name, const int8_t* p, uint32_t n, int width) { dbg_copy(c, name, p, size_t(n) * width); }
 
-  // Upsampling + Pruning from depth k to k+1 (Eq.6/9/11).  Default: the dp4a kernel
-  // that computes only the kept child blocks (measured faster: 4.5 vs 6.4 ms per
-  // B=256 step); PCC_UP=tc selects the tcgen05 variant (bit-exact, same contract).
+  // Upsampling + Pruning from depth k to k+1 (Eq.6/9/11).  C = 32: the tcgen05 kernel
+  // (up_tc.cu; 2.1 vs 4.5 ms per B=256 step for the dp4a kernel); PCC_UP=simt selects the
+  // dp4a kernel (bit-exact, same contract; also the path for C != 32).
   void up(int k, const int8_t* S, const DUp& L, int8_t* dst) {
-    static const bool tcv = [] {
+    static const bool simt = [] {
       const char* e = getenv("PCC_UP");
-      return e && std::string(e) == "tc";
+      return e && std::string(e) == "simt";
     }();
-    if (C == 32 && tcv)
+    if (C == 32 && !simt)
       up_prune_tc(c, S, X(k), par() + o.nb[k + 1], key() + o.nb[k + 1], o.N[k + 1], L, dst);
     else
       up_prune(c, S, X(k), par() + o.nb[k + 1], key() + o.nb[k + 1], o.N[k + 1], C, L, dst);

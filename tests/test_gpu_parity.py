@@ -256,6 +256,65 @@ def test_large_level_multi_segment(pcc, ctx):
     assert np.array_equal(dec[0], morton_sorted_unique(pts, 12))
 
 
+def _map_rqs(obj, fn):
+    """Apply fn to every activation requant of a Model (the logit requant is separate)."""
+    import dataclasses
+    seen = set()
+
+    def walk(o):
+        if isinstance(o, list):
+            for v in o:
+                walk(v)
+        elif isinstance(o, dict):
+            for v in o.values():
+                walk(v)
+        elif dataclasses.is_dataclass(o) and not isinstance(o, I.RQ):
+            for fl in dataclasses.fields(o):
+                v = getattr(o, fl.name)
+                if isinstance(v, I.RQ):
+                    if fl.name != "rq_logit" and id(v) not in seen:
+                        seen.add(id(v))
+                        fn(v)
+                else:
+                    walk(v)
+    walk(obj)
+    return len(seen)
+
+
+@pytest.mark.parametrize("form", ["generic", "abs"])
+@pytest.mark.parametrize("C,cfg", [(32, "cfg2"), (8, "cfg1")])
+def test_requant_forms(pcc, ctx, form, C, cfg):
+    """The three device forms of Eq.14's requant (rq.cuh) against the oracle: the default
+    model takes the signed one-multiply form; r > 32 forces the generic 64-bit form
+    (same real multipliers as the default model), m >= 2^(r-1) the
+    |x| form (saturating layers)."""
+    model = I.make_model(C=C, H=C, seed=3, min_depth=9, max_depth=18)
+
+    def generic(q):  # r' = 33 > 32, m' = m * 2^(33 - r): the same real multiplier
+        k = 33 - q.r
+        assert k >= 0 and (q.m_pos << k) < 2**31 and (q.m_neg << k) < 2**31
+        q.m_pos, q.m_neg, q.r = q.m_pos << k, q.m_neg << k, 33
+
+    def absform(q):
+        q.m_pos, q.m_neg, q.r = int(0.6 * (1 << 24)), int(0.15 * (1 << 24)), 24
+
+    assert _map_rqs(model, generic if form == "generic" else absform) > 10
+    mb = model.to_bytes()
+    om = O.Model(mb)
+    m = pcc.pcc_model_load(mb, 0)
+    try:
+        sc = I.CONFIGS[cfg]
+        frames = I.make_frames(sc, 2, first=5)
+        got, _ = gpu_encode(pcc, ctx, m, frames, sc.bit_depth)
+        for f, g in zip(frames, got):
+            assert g == O.encode(om, f, sc.bit_depth)
+        dec = gpu_decode(pcc, ctx, m, got, sum(len(f) for f in frames))
+        for f, x in zip(frames, dec):
+            assert np.array_equal(x, morton_sorted_unique(f, sc.bit_depth))
+    finally:
+        pcc.pcc_model_destroy(m)
+
+
 # ---------------------------------------------------------------------------------------
 # errors and robustness
 # ---------------------------------------------------------------------------------------
@@ -324,7 +383,7 @@ print("ALT-OK")
 """
 
 
-@pytest.mark.parametrize("env", [{"PCC_UP": "tc"}, {"PCC_HEAD": "simt", "PCC_CONV": "simt"}])
+@pytest.mark.parametrize("env", [{"PCC_UP": "simt"}, {"PCC_HEAD": "simt", "PCC_CONV": "simt"}])
 def test_alternate_kernels_bit_exact(pcc, env):
     import os
     import subprocess
