@@ -14,8 +14,8 @@
 // copy of W_X in smem, the bias a padded smem row; requant in the signed one-multiply
 // form (rq.cuh) and two 16-byte stores of the child row j.  Four independent 128-thread
 // tile groups per CTA (own A tile, TMEM accumulator, mbarrier, named barrier) overlap
-// one another's gathers, MMAs and epilogues; the next tile's par/key/X are prefetched
-// into registers during the current epilogue.
+// one another's gathers, MMAs and epilogues; within a group the indices run two tiles
+// ahead in registers and the next tile's gather is in flight during this epilogue.
 #include "pcc_internal.cuh"
 #include "rq.cuh"
 #include "tc.cuh"
@@ -90,17 +90,22 @@ __global__ void __launch_bounds__(UNT, 1) k_up_tc(const int8_t* __restrict__ S, 
       xx = Xp[pp];
     }
   };
+  auto gather = [&](uint32_t pp, uint32_t c_) {  // the parent row into K-slot c_ of row r
+    cp16(sA + c_ * 4096 + tc::kmaj_off(r, 0), S + size_t(pp) * 32);
+    cp16(sA + c_ * 4096 + tc::kmaj_off(r, 16), S + size_t(pp) * 32 + 16);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  // software pipeline: indices two tiles ahead in registers, the next tile's gather in
+  // flight during this tile's epilogue
+  uint32_t pn = 0, cn = 0, xn = 0;
   fetch(tile, p, cc, x);
+  fetch(tile + stride, pn, cn, xn);
+  if (x) gather(p, cc);
   for (; tile < ntiles; tile += stride) {
-    // gather: the parent row into K-slot c of row r
-    if (x) {
-      cp16(sA + cc * 4096 + tc::kmaj_off(r, 0), S + size_t(p) * 32);
-      cp16(sA + cc * 4096 + tc::kmaj_off(r, 16), S + size_t(p) * 32 + 16);
-    }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     tc::fence_async_smem();
     tc::fence_before();
-    bar_group(1 + g);
+    bar_group(1 + g);  // A tile complete (gathers + restored zeros), TMEM reads of the last tile done
     tc::fence_after();
     if (r == 0) {
 #pragma unroll
@@ -109,19 +114,21 @@ __global__ void __launch_bounds__(UNT, 1) k_up_tc(const int8_t* __restrict__ S, 
                    tc::sdesc(tc::smem_u32(sm + SM_B + c * 1024)), IDESC_UP, c > 0 ? 1u : 0u);
       tc::commit(mbar);
     }
-    // prefetch the next tile's indices while the MMAs run
-    uint32_t pn = 0, cn = 0, xn = 0;
-    fetch(tile + stride, pn, cn, xn);
+    uint32_t p2 = 0, c2 = 0, x2 = 0;
+    fetch(tile + 2 * stride, p2, c2, x2);
     tc::mbar_wait(mbar, phase);
     phase ^= 1u;
     tc::fence_after();
     uint32_t v[32];
     tc::tmem_ld32(tacc, v);
     tc::tmem_wait_ld();
-    if (x) {
-      // the MMAs have consumed the tile: restore the zero slot
+    // the MMAs have consumed the tile: restore the zero slot, start the next gather
+    if (x && !(xn && cn == cc)) {
       *reinterpret_cast<uint4*>(sA + cc * 4096 + tc::kmaj_off(r, 0)) = make_uint4(0u, 0u, 0u, 0u);
       *reinterpret_cast<uint4*>(sA + cc * 4096 + tc::kmaj_off(r, 16)) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (xn) gather(pn, cn);
+    if (x) {
       const uint4* wx4 = reinterpret_cast<const uint4*>(sWX + (x - 1) * WXS + 32 * cc);
       const uint4 wa = wx4[0], wb = wx4[1];
       const uint32_t wxw[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
@@ -145,12 +152,8 @@ __global__ void __launch_bounds__(UNT, 1) k_up_tc(const int8_t* __restrict__ S, 
       dst[0] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
       dst[1] = make_uint4(o4[4], o4[5], o4[6], o4[7]);
     }
-    p = pn;
-    cc = cn;
-    x = xn;
-    tc::fence_before();
-    bar_group(1 + g);  // TMEM accumulator and A tile are reused by the next tile
-    tc::fence_after();
+    p = pn, cc = cn, x = xn;
+    pn = p2, cn = c2, xn = x2;
   }
   __syncthreads();
   if (t < 32) tc::tmem_dealloc<32 * UG>(*thold);
