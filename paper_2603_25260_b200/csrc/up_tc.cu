@@ -14,8 +14,8 @@
 // copy of W_X in smem, the bias a padded smem row; requant in the signed one-multiply
 // form (rq.cuh) and two 16-byte stores of the child row j.  Four independent 128-thread
 // tile groups per CTA (own A tile, TMEM accumulator, mbarrier, named barrier) overlap
-// one another's gathers, MMAs and epilogues; within a group the indices run two tiles
-// ahead in registers and the next tile's gather is in flight during this epilogue.
+// one another's gathers, MMAs and epilogues; within a group a software pipeline keeps
+// the index loads three tiles and the code loads two tiles ahead of the epilogue.
 #include "pcc_internal.cuh"
 #include "rq.cuh"
 #include "tc.cuh"
@@ -33,12 +33,16 @@ constexpr int BST = 36;           // bias row stride in int32 (32 + 4: distinct 
 __device__ __forceinline__ void cp16(void* s, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(s)), "l"(g));
 }
+__device__ __forceinline__ void cp4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(tc::smem_u32(s)), "l"(g));
+}
 __device__ __forceinline__ void bar_group(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 
 // smem: per group an A tile [128 x 256] (8 canonical slabs of 4 KB); B = 8 slabs [32 x 32];
 // W_X^T [255][272] int8; bias [8][36] int32; mbarriers + TMEM holder
 constexpr int SM_A = 0, SM_B = UG * 32768, SM_WX = SM_B + 8192, SM_BIAS = SM_WX + NCODE * WXS;
-constexpr int SM_MBAR = SM_BIAS + 8 * BST * 4, SM_END = SM_MBAR + 8 * UG + 16;
+constexpr int SM_RING = SM_BIAS + 8 * BST * 4;  // per group [3 slots][par | key low word][128] u32
+constexpr int SM_MBAR = SM_RING + UG * 3 * 256 * 4, SM_END = SM_MBAR + 8 * UG + 16;
 
 template <bool SIGNED>
 __global__ void __launch_bounds__(UNT, 1) k_up_tc(const int8_t* __restrict__ S, const uint8_t* __restrict__ Xp,
@@ -79,28 +83,34 @@ __global__ void __launch_bounds__(UNT, 1) k_up_tc(const int8_t* __restrict__ S, 
   const uint32_t stride = gridDim.x * UG;
   uint32_t tile = blockIdx.x * UG + g;
   uint32_t phase = 0;
-  // current tile's child: parent, child index, parent code (0 = no child row)
-  uint32_t p = 0, cc = 0, x = 0;
-  auto fetch = [&](uint32_t tl, uint32_t& pp, uint32_t& c_, uint32_t& xx) {
-    const uint32_t j = tl * 128 + r;
-    xx = 0;
-    if (tl < ntiles && j < nc) {
-      pp = par[j];
-      c_ = uint32_t(key[j]) & 7u;
-      xx = Xp[pp];
+  // Software pipeline per thread (row r of its group's tiles T, T+s, T+2s, ...): the
+  // indices par/key of tile T+3s are copied (cp.async) into a 3-slot ring while tile T is
+  // processed, the parent code X of tile T+2s is loaded into a register, and the gather of
+  // tile T+s is in flight during the epilogue of T.  Each thread reads only its own ring
+  // entries, so the ring needs no barrier.
+  uint32_t* ring = reinterpret_cast<uint32_t*>(sm + SM_RING) + g * 768;
+  auto valid = [&](uint32_t tl) { return tl < ntiles && tl * 128 + r < nc; };
+  auto idx_load = [&](uint32_t tl, int slot) {
+    if (valid(tl)) {
+      cp4(ring + slot * 256 + r, par + tl * 128 + r);
+      cp4(ring + slot * 256 + 128 + r, reinterpret_cast<const uint32_t*>(key + tl * 128 + r));
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
   auto gather = [&](uint32_t pp, uint32_t c_) {  // the parent row into K-slot c_ of row r
     cp16(sA + c_ * 4096 + tc::kmaj_off(r, 0), S + size_t(pp) * 32);
     cp16(sA + c_ * 4096 + tc::kmaj_off(r, 16), S + size_t(pp) * 32 + 16);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  // software pipeline: indices two tiles ahead in registers, the next tile's gather in
-  // flight during this tile's epilogue
-  uint32_t pn = 0, cn = 0, xn = 0;
-  fetch(tile, p, cc, x);
-  fetch(tile + stride, pn, cn, xn);
-  if (x) gather(p, cc);
+  idx_load(tile, 0);
+  idx_load(tile + stride, 1);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  bool v = valid(tile), vn = valid(tile + stride);
+  uint32_t cc = v ? (ring[128 + r] & 7u) : 0u, x = v ? uint32_t(Xp[ring[r]]) : 0u;
+  uint32_t cn = vn ? (ring[256 + 128 + r] & 7u) : 0u, xn = vn ? uint32_t(Xp[ring[256 + r]]) : 0u;
+  if (v) gather(ring[r], cc);
+  idx_load(tile + 2 * stride, 2);
+  int slot = 0;
   for (; tile < ntiles; tile += stride) {
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     tc::fence_async_smem();
@@ -114,21 +124,25 @@ __global__ void __launch_bounds__(UNT, 1) k_up_tc(const int8_t* __restrict__ S, 
                    tc::sdesc(tc::smem_u32(sm + SM_B + c * 1024)), IDESC_UP, c > 0 ? 1u : 0u);
       tc::commit(mbar);
     }
-    uint32_t p2 = 0, c2 = 0, x2 = 0;
-    fetch(tile + 2 * stride, p2, c2, x2);
+    const int s1 = slot == 2 ? 0 : slot + 1, s2 = s1 == 2 ? 0 : s1 + 1;
+    // tile T+2s: indices landed (waited above) -> its code; then tile T+3s's indices into T's slot
+    const bool v2 = valid(tile + 2 * stride);
+    const uint32_t c2 = v2 ? (ring[s2 * 256 + 128 + r] & 7u) : 0u;
+    const uint32_t x2 = v2 ? uint32_t(Xp[ring[s2 * 256 + r]]) : 0u;
+    idx_load(tile + 3 * stride, slot);
     tc::mbar_wait(mbar, phase);
     phase ^= 1u;
     tc::fence_after();
-    uint32_t v[32];
-    tc::tmem_ld32(tacc, v);
+    uint32_t acc[32];
+    tc::tmem_ld32(tacc, acc);
     tc::tmem_wait_ld();
     // the MMAs have consumed the tile: restore the zero slot, start the next gather
-    if (x && !(xn && cn == cc)) {
+    if (v && !(vn && cn == cc)) {
       *reinterpret_cast<uint4*>(sA + cc * 4096 + tc::kmaj_off(r, 0)) = make_uint4(0u, 0u, 0u, 0u);
       *reinterpret_cast<uint4*>(sA + cc * 4096 + tc::kmaj_off(r, 16)) = make_uint4(0u, 0u, 0u, 0u);
     }
-    if (xn) gather(pn, cn);
-    if (x) {
+    if (vn) gather(ring[s1 * 256 + r], cn);
+    if (v) {
       const uint4* wx4 = reinterpret_cast<const uint4*>(sWX + (x - 1) * WXS + 32 * cc);
       const uint4 wa = wx4[0], wb = wx4[1];
       const uint32_t wxw[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
@@ -137,10 +151,10 @@ __global__ void __launch_bounds__(UNT, 1) k_up_tc(const int8_t* __restrict__ S, 
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int4 bb = b4[k];
-        int32_t a0 = __dp4a(int32_t(wxw[k]), qm0, int32_t(v[4 * k]) + bb.x);
-        int32_t a1 = __dp4a(int32_t(wxw[k]), qm1, int32_t(v[4 * k + 1]) + bb.y);
-        int32_t a2 = __dp4a(int32_t(wxw[k]), qm2, int32_t(v[4 * k + 2]) + bb.z);
-        int32_t a3 = __dp4a(int32_t(wxw[k]), qm3, int32_t(v[4 * k + 3]) + bb.w);
+        int32_t a0 = __dp4a(int32_t(wxw[k]), qm0, int32_t(acc[4 * k]) + bb.x);
+        int32_t a1 = __dp4a(int32_t(wxw[k]), qm1, int32_t(acc[4 * k + 1]) + bb.y);
+        int32_t a2 = __dp4a(int32_t(wxw[k]), qm2, int32_t(acc[4 * k + 2]) + bb.z);
+        int32_t a3 = __dp4a(int32_t(wxw[k]), qm3, int32_t(acc[4 * k + 3]) + bb.w);
         if (SIGNED) {
           o4[k] = pack_sat4(rq_s(a0, rq), rq_s(a1, rq), rq_s(a2, rq), rq_s(a3, rq));
         } else {
@@ -152,8 +166,9 @@ __global__ void __launch_bounds__(UNT, 1) k_up_tc(const int8_t* __restrict__ S, 
       dst[0] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
       dst[1] = make_uint4(o4[4], o4[5], o4[6], o4[7]);
     }
-    p = pn, cc = cn, x = xn;
-    pn = p2, cn = c2, xn = x2;
+    v = vn, cc = cn, x = xn;
+    vn = v2, cn = c2, xn = x2;
+    slot = s1;
   }
   __syncthreads();
   if (t < 32) tc::tmem_dealloc<32 * UG>(*thold);
