@@ -150,12 +150,25 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         for (int hh = 0; hh < HQ; ++hh) ad[hh] = int8_t(ab[hh >> 2] >> (8 * (hh & 3)));
       }
     }
+    // the logit bias b2 initialises the accumulator (columns 64q.. of row r): the MMA adds
+    // a W2^T onto it, so the passes below read z = b2 + a W2^T directly
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+      uint32_t bv[16];
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const uint4 b4 = *reinterpret_cast<const uint4*>(sb2 + 64 * q + 16 * ch + 4 * k4);
+        bv[4 * k4] = b4.x, bv[4 * k4 + 1] = b4.y, bv[4 * k4 + 2] = b4.z, bv[4 * k4 + 3] = b4.w;
+      }
+      tmem_st16(taddr + ch * 16, bv);
+    }
+    tmem_wait_st();
     tc::fence_async_smem();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     if (tid == 0) {
-      tc::mma_i8(tbase, adesc, bdesc, IDESC, 0u);
+      tc::mma_i8(tbase, adesc, bdesc, IDESC, 1u);
       tc::commit(mbar);
     }
     tc::mbar_wait(mbar, phase);
@@ -170,14 +183,14 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       uint32_t v[16];
       tmem_ld16(taddr + ch * 16, v);
       tc::tmem_wait_ld();
+      const bool pad = q == 3 && ch == 3;  // column 255 is padding, not a symbol
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int i = 64 * q + ch * 16 + k;
-        if (i < NCODE) {
-          zmax = max(zmax, int32_t(v[k]) + sb2[i]);
-          if (SAT) zmin = min(zmin, int32_t(v[k]) + sb2[i]);
-        }
+      for (int k = 0; k < 15; ++k) {
+        zmax = max(zmax, int32_t(v[k]));
+        if (SAT) zmin = min(zmin, int32_t(v[k]));
       }
+      zmax = max(zmax, pad ? INT32_MIN : int32_t(v[15]));
+      if (SAT) zmin = min(zmin, pad ? INT32_MAX : int32_t(v[15]));
     }
     red[(q * TILE + r) * 2] = zmax;
     red[(q * TILE + r) * 2 + 1] = zmin;
@@ -191,36 +204,50 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     // ---- pass 2: Q8 logit, e = LUT[delta >> 2] (0 beyond 16 nats), local sum and
     //      local first index with delta == 0 (e stored back into TMEM) ----
     uint32_t ssum = 0;
-    int ist = 1 << 30;
+    uint32_t kmin = 0xffffffffu;  // min over (min(delta, 4096) << 8) + i: the first i with delta == 0
     const int64_t lm = rql.mp;
     const int lr = rql.r;
+    // one-multiply form (rq.cuh, signed): delta = mu - lq(z) = hi32(z * (-M) + mu 2^32 + 2^31 - 1)
+    const bool fastl = rql.fast_s && nosat;
+    const int32_t nM = -rql.Sp;
+    const int64_t C2 = (int64_t(mu) << 32) + 0x7fffffff;
 #pragma unroll 1
     for (int ch = 0; ch < 4; ++ch) {
       uint32_t v[16];
       tmem_ld16(taddr + ch * 16, v);
       tc::tmem_wait_ld();
+      uint32_t kc = 0xffffffffu;
+      if (fastl) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int i = 64 * q + ch * 16 + k;
-        const int32_t zz = int32_t(v[k]) + sb2[i];
-        // lq8(zz) without the 64-bit clamp: saturation is decided in the z domain and
-        // selected (branch-free) over the low word of the 64-bit shift; rows whose
-        // [zmin, zmax] lies inside the thresholds skip the selects
-        int32_t lv = int32_t((int64_t(zz) * lm + lhalf) >> lr);
-        if (SAT && !nosat) {
-          lv = zz > zsat_hi ? (1 << 24) : lv;
-          lv = zz < zsat_lo ? -(1 << 24) : lv;
+        for (int k = 0; k < 16; ++k) {
+          const uint32_t dl = uint32_t(int32_t((int64_t(int32_t(v[k])) * nM + C2) >> 32));
+          const uint32_t dc = min(dl, 4096u);
+          kc = min(kc, (dc << 8) + uint32_t(k));
+          v[k] = sLut[dc];  // LUT4[4096] = 0: delta >= 4096
         }
-        const uint32_t dl = uint32_t(mu - lv);
-        const uint32_t e = sLut[min(dl, 4096u)];  // LUT4[4096] = 0: delta >= 4096
-        if (dl == 0u) ist = min(ist, i);  // i increases: the first index wins
-        v[k] = e;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int32_t zz = int32_t(v[k]);
+          // lq8(zz) without the 64-bit clamp: saturation is decided in the z domain and
+          // selected (branch-free) over the low word of the 64-bit shift
+          int32_t lv = int32_t((int64_t(zz) * lm + lhalf) >> lr);
+          if (SAT && !nosat) {
+            lv = zz > zsat_hi ? (1 << 24) : lv;
+            lv = zz < zsat_lo ? -(1 << 24) : lv;
+          }
+          const uint32_t dc = min(uint32_t(mu - lv), 4096u);
+          kc = min(kc, (dc << 8) + uint32_t(k));
+          v[k] = sLut[dc];
+        }
       }
+      kmin = min(kmin, kc + uint32_t(64 * q + ch * 16));
       if (q == 3 && ch == 3) v[15] = 0u;  // column 255 is padding, not a symbol
 #pragma unroll
       for (int k = 0; k < 16; ++k) ssum += v[k];
       tmem_st16(taddr + ch * 16, v);
     }
+    const int ist = int(kmin < 256u ? kmin : (1u << 30));
     __syncthreads();  // everyone has read red (pass-1 values) before it is overwritten
     red[(q * TILE + r) * 2] = int32_t(ssum);
     red[(q * TILE + r) * 2 + 1] = ist;
@@ -347,15 +374,17 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
           const int isr = ri[5];
           const uint4 g = *reinterpret_cast<const uint4*>(stage + rr * STG + 8 * j);
           const uint32_t in[4] = {g.x, g.y, g.z, g.w};
+          // packed u16 pairs: every cdf value below index 255 is < 2^16, so adding the
+          // quarter offset and the leftover to both halves at once never carries across
+          const uint32_t offw = off * 0x10001u, leftw = left * 0x10001u;
           uint32_t o[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int i0 = int(8 * j) + 2 * u;
-            const uint32_t c0 = (in[u] & 0xffffu) + off + (i0 > isr ? left : 0u);
-            uint32_t c1 = (in[u] >> 16) + off + (i0 + 1 > isr ? left : 0u);
-            if (i0 + 1 >= NCODE) c1 = 0xffffu;
-            o[u] = (c0 & 0xffffu) | (c1 << 16);
+            const uint32_t ext = i0 > isr ? leftw : (i0 == isr ? (left << 16) : 0u);
+            o[u] = in[u] + offw + ext;
           }
+          if (j == 31u) o[3] = (o[3] & 0xffffu) | 0xffff0000u;  // index 255: padding
           reinterpret_cast<uint4*>(cdf + size_t(tile * TILE + rr) * 256)[j] = make_uint4(o[0], o[1], o[2], o[3]);
         }
       }
