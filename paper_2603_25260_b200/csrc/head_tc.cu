@@ -68,7 +68,8 @@ struct SmemLayout {
   static constexpr int RED = MBAR + 16;          // [4][128] x (a, b) int32 = 4 KB
   static constexpr int ROWI = RED + 4096;        // [128] x 8 int32 = 4 KB
   static constexpr int STAGE = ROWI + 4096;      // decoder: 128 x STG u16 (66 KB)
-  static constexpr int END = STAGE + TILE * STG * 2;
+  static constexpr int MASK = STAGE + TILE * STG * 2;  // decoder: [9][4] u32 leftover masks
+  static constexpr int END = MASK + 9 * 16;
 };
 
 // SAT = false when the model proves |z| can never reach the logit saturation thresholds
@@ -110,6 +111,10 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   for (int k = tid; k < 256; k += NT) sb2[k] = b2[k];
   for (int k = tid; k < H * CW; k += NT) sW1[k] = reinterpret_cast<const int32_t*>(W1)[k];
   for (int k = tid; k < H; k += NT) sb1[k] = b1[k];
+  if (MODE == 1 && tid < 36) {  // MASK[t][u]: halves of word u (chunk elements 2u, 2u+1) with index >= t
+    const int t = tid >> 2, u = tid & 3;
+    reinterpret_cast<uint32_t*>(sm + S::MASK)[tid] = (2 * u >= t ? 0x0000ffffu : 0u) | (2 * u + 1 >= t ? 0xffff0000u : 0u);
+  }
   if (warp == 0) tc::tmem_alloc<256>(thold);
   if (tid == 0) tc::mbar_init(mbar, 1);
   tc::fence_async_smem();
@@ -361,32 +366,30 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         rowi[r * 8 + 5] = istar;
       }
       __syncthreads();
-      // coalesced write-out: 16 rows per iteration, 32 threads x 16 bytes per 512-byte row;
-      // adds the quarter offset and, after the first argmax, the leftover
+      // coalesced write-out: 16 rows per iteration, 32 threads x 16 bytes per 512-byte row.
+      // Packed u16 pairs: every cdf value below index 255 is < 2^16, so the quarter offset
+      // and the leftover are added to both halves at once without carries; the leftover
+      // goes to the elements after the first argmax: t = how many of the chunk's 8
+      // elements are <= istar selects the half-word mask of each word.
       const uint32_t rows_here = (n - tile * TILE) < uint32_t(TILE) ? (n - tile * TILE) : uint32_t(TILE);
-      const uint32_t j = uint32_t(tid) & 31u, sub = uint32_t(tid) >> 5;
-      for (uint32_t rb = 0; rb < rows_here; rb += 16) {
-        const uint32_t rr = rb + sub;
-        if (rr < rows_here) {
-          const int32_t* ri = rowi + rr * 8;
-          const uint32_t off = uint32_t(ri[j >> 3]);
-          const uint32_t left = uint32_t(ri[4]);
-          const int isr = ri[5];
-          const uint4 g = *reinterpret_cast<const uint4*>(stage + rr * STG + 8 * j);
-          const uint32_t in[4] = {g.x, g.y, g.z, g.w};
-          // packed u16 pairs: every cdf value below index 255 is < 2^16, so adding the
-          // quarter offset and the leftover to both halves at once never carries across
-          const uint32_t offw = off * 0x10001u, leftw = left * 0x10001u;
-          uint32_t o[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i0 = int(8 * j) + 2 * u;
-            const uint32_t ext = i0 > isr ? leftw : (i0 == isr ? (left << 16) : 0u);
-            o[u] = in[u] + offw + ext;
-          }
-          if (j == 31u) o[3] = (o[3] & 0xffffu) | 0xffff0000u;  // index 255: padding
-          reinterpret_cast<uint4*>(cdf + size_t(tile * TILE + rr) * 256)[j] = make_uint4(o[0], o[1], o[2], o[3]);
-        }
+      const uint32_t j = uint32_t(tid) & 31u, sub = uint32_t(tid) >> 5, jq = j >> 3;
+      const uint4* mask4 = reinterpret_cast<const uint4*>(sm + S::MASK);
+      const uint16_t* sp = stage + sub * STG + 8 * j;
+      const int32_t* rp = rowi + sub * 8;
+      uint4* gp = reinterpret_cast<uint4*>(cdf + (size_t(tile) * TILE + sub) * 256) + j;
+      for (uint32_t rr = sub; rr < rows_here; rr += 16, sp += 16 * STG, rp += 16 * 8, gp += 16 * 32) {
+        const uint32_t offw = uint32_t(rp[jq]) * 0x10001u;
+        const int2 li = *reinterpret_cast<const int2*>(rp + 4);  // leftover, first argmax
+        const uint32_t leftw = uint32_t(li.x) * 0x10001u;
+        const uint4 m = mask4[min(max(li.y + 1 - int(8 * j), 0), 8)];
+        const uint4 g = *reinterpret_cast<const uint4*>(sp);
+        uint4 o;
+        o.x = g.x + offw + (leftw & m.x);
+        o.y = g.y + offw + (leftw & m.y);
+        o.z = g.z + offw + (leftw & m.z);
+        o.w = g.w + offw + (leftw & m.w);
+        if (j == 31u) o.w = (o.w & 0xffffu) | 0xffff0000u;  // index 255: padding
+        *gp = o;
       }
     }
     tc::fence_before();
