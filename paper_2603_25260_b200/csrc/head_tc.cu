@@ -270,14 +270,17 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     // S <= 2^31: the remainder r = e*65281 - q_est*S lies in [0, 2S) subset [0, 2^32), so
     // the correction is exact in 32-bit wrap-around arithmetic; otherwise use 64 bits.
     const bool s32 = Ssum <= 0x80000000u;
+    const uint32_t nS = 0u - Ssum;
     // p = 1 + q for the 16 exponentials of a chunk (the s32 choice is per row, hoisted
     // out of the element loop so only one variant is issued)
     auto pchunk = [&](uint32_t (&v)[16]) {
       if (s32) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
+          // t = e*65281 - (q_est + 1) S = remainder - S in [-S, S): q = q_est + (t >= 0)
           const uint32_t qt = __umulhi(v[k], inv32);
-          v[k] = 1u + qt + ((v[k] * 65281u - qt * Ssum) >= Ssum ? 1u : 0u);
+          const uint32_t t = v[k] * 65281u + qt * nS + nS;
+          v[k] = qt + 1u + (~t >> 31);
         }
       } else {
 #pragma unroll
