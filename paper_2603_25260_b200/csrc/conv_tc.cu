@@ -242,15 +242,30 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
           const int4 a0 = s4[0], a1 = s4[1];
           const uint32_t sw[8] = {uint32_t(a0.x), uint32_t(a0.y), uint32_t(a0.z), uint32_t(a0.w),
                                   uint32_t(a1.x), uint32_t(a1.y), uint32_t(a1.z), uint32_t(a1.w)};
+          if (k_s >= -128 && k_s <= 127) {  // k_s * byte o%4 of word o/4 as one dp4a
+            const int32_t m0 = k_s & 0xff;
+            const int32_t km[4] = {m0, m0 << 8, m0 << 16, int32_t(uint32_t(m0) << 24)};
 #pragma unroll
-          for (int o = 0; o < 32; ++o) acc[o] += k_s * int32_t(int8_t(sw[o >> 2] >> (8 * (o & 3))));
+            for (int o = 0; o < 32; ++o) acc[o] = __dp4a(int32_t(sw[o >> 2]), km[o & 3], acc[o]);
+          } else {
+#pragma unroll
+            for (int o = 0; o < 32; ++o) acc[o] += k_s * int32_t(int8_t(sw[o >> 2] >> (8 * (o & 3))));
+          }
         }
+        if (rq.fast_s) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          uint32_t pk = 0;
+          for (int k = 0; k < 8; ++k)
+            w[k] = pack_sat4(rq_s(acc[4 * k] + sbias[4 * k], rq), rq_s(acc[4 * k + 1] + sbias[4 * k + 1], rq),
+                             rq_s(acc[4 * k + 2] + sbias[4 * k + 2], rq), rq_s(acc[4 * k + 3] + sbias[4 * k + 3], rq));
+        } else {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) pk |= (uint32_t(rq8(acc[4 * k + u] + sbias[4 * k + u], rq)) & 0xffu) << (8 * u);
-          w[k] = pk;
+          for (int k = 0; k < 8; ++k) {
+            uint32_t pk = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              pk |= (uint32_t(rq8(acc[4 * k + u] + sbias[4 * k + u], rq)) & 0xffu) << (8 * u);
+            w[k] = pk;
+          }
         }
       } else {
 #pragma unroll

@@ -137,13 +137,23 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
 #pragma unroll
       for (int w = 0; w < CW; ++w) fw[w] = valid ? reinterpret_cast<const int32_t*>(F + size_t(row) * C)[w] : 0;
       uint32_t ab[2] = {0u, 0u};
+      int32_t hacc[HQ];
 #pragma unroll
       for (int hh = 0; hh < HQ; ++hh) {
         const int h = q * HQ + hh;
         int32_t acc = sb1[h];
 #pragma unroll
         for (int w = 0; w < CW; ++w) acc = __dp4a(fw[w], sW1[h * CW + w], acc);
-        ab[hh >> 2] |= (uint32_t(rq8(acc, rq1)) & 0xffu) << (8 * (hh & 3));
+        hacc[hh] = acc;
+      }
+      if (HQ % 4 == 0 && rq1.fast_s) {
+#pragma unroll
+        for (int g4 = 0; g4 < HQ / 4; ++g4)
+          ab[g4] = pack_sat4(rq_s(hacc[4 * g4], rq1), rq_s(hacc[4 * g4 + 1], rq1), rq_s(hacc[4 * g4 + 2], rq1),
+                             rq_s(hacc[4 * g4 + 3], rq1));
+      } else {
+#pragma unroll
+        for (int hh = 0; hh < HQ; ++hh) ab[hh >> 2] |= (uint32_t(rq8(hacc[hh], rq1)) & 0xffu) << (8 * (hh & 3));
       }
       uint8_t* dst = sA + tc::kmaj_off(r, q * HQ);
       if constexpr (HQ == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(ab[0], ab[1]);

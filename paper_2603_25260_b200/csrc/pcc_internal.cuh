@@ -206,6 +206,10 @@ void gemm_i8_test(pcc_ctx c, const int8_t* dA, const int8_t* dB, int N, int32_t*
 void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* par_c, const uint64_t* key_c,
                  uint32_t nc, const DUp& L, int8_t* out);
 
+// ---- down_tc.cu (K2S2 downsampling as a block-diagonal tcgen05 product; C = 32) ----
+void down_tc(pcc_ctx c, const int8_t* g, const uint8_t* Xp, const uint32_t* cs_p, uint32_t np, const DDown& L,
+             int8_t* out);
+
 // ---- conv_tc.cu (gather -> tcgen05 kind::i8 per kernel offset; C = 32) ----
 void conv3_tc(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,
               int skip_mode, const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out);

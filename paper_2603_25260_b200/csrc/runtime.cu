@@ -451,7 +451,15 @@ struct Net {
     dbgF(nm("G", d, d - 1), ga, o.N[d - 1], C);
     for (int s = 0; s < j - 1; ++s) {
       const int k = d - 1 - s;  // depth k -> k-1
-      down(c, ga, X(k - 1), cs() + o.nb[k - 1], o.N[k - 1], C, dp.down[s], gb);
+      // C = 32: the tcgen05 kernel (down_tc.cu); PCC_DOWN=simt selects the dp4a kernel
+      static const bool simt = [] {
+        const char* e = getenv("PCC_DOWN");
+        return e && std::string(e) == "simt";
+      }();
+      if (C == 32 && !simt)
+        down_tc(c, ga, X(k - 1), cs() + o.nb[k - 1], o.N[k - 1], dp.down[s], gb);
+      else
+        down(c, ga, X(k - 1), cs() + o.nb[k - 1], o.N[k - 1], C, dp.down[s], gb);
       std::swap(ga, gb);
       dbgF(nm("G", d, k - 1), ga, o.N[k - 1], C);
     }
