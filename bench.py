@@ -124,6 +124,12 @@ def oracle_rate(frames, L, model_bytes, threads: int):
     return len(frames) / dt, dt
 
 
+def run_config(B, world):
+    """The workload both arms report (identical dicts: the driver compares like with like)."""
+    return {"workload": WORKLOAD, "frames_per_gpu_per_step": B, "global_batch": B * world,
+            "parallelism": f"frames/dp{world}", "l2": "flushed between steps (256 MiB write, outside the events)"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -143,9 +149,10 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64 (scalar CPU)",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "frames_per_step": cores},
+            "data": "synthetic", "config": run_config(args.batch, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"{cores} cfg2 frames per step (encode+decode), one frame per thread"},
+                             "sample": f"each step a bounded sample of the workload: {cores} of its cfg2 frames "
+                                       f"(encode+decode), one frame per thread"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -203,12 +210,14 @@ ALU_OPS_PER_NODE = {"head_enc": 32 * 32 / 4 + 12 * 255, "head_dec": 32 * 32 / 4 
 
 
 def measured_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+    """(DRAM bytes, note) of the longest launch of `kernel` from the committed ncu --set full
+    summary (profiles/traffic.json, written by tools/summarize_round.py), if any."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(p)).get(kernel)
+        t = json.load(open(p))[kernel]
+        return t["dram_bytes_per_launch"], f"dram read+write of the {t['launch']} ({t['duration']}), {t['source']}"
     except Exception:
-        return None
+        return None, None
 
 
 def run_ours(args, rank, world, dist):
@@ -407,38 +416,40 @@ def run_ours(args, rank, world, dist):
     if top[0]:
         name, v = top
         sec = v["ms_per_step"] / 1e3
-        traffic = measured_traffic(name)
+        traffic, traffic_note = measured_traffic(name)
         if name in ALU_OPS_PER_NODE:
             # integer-ALU bound: algorithmic ops per coded node x coded nodes per step
             sm_max = float(pk.get("sm_max_mhz", 1965.0))
             achieved = coded_per_step * ALU_OPS_PER_NODE[name] / sec / 1e12
             peak = 148 * 4 * 32 * sm_max * 1e6 / 1e12
             roof = {"kernel": name, "bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                    "frac": achieved / peak, "traffic": traffic, "peak_src": ALU_PEAK_NOTE,
+                    "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note, "peak_src": ALU_PEAK_NOTE,
                     "launches_per_step": v["launches_per_step"], "share_of_step": v["ms_per_step"] / prof_total}
         else:
             achieved = v["bytes_per_step"] / sec / 1e9
             peak = float(pk["hbm_gbs"])
             roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": traffic, "peak_src": pk_src + " copy bandwidth",
+                    "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
+                    "peak_src": pk_src + " copy bandwidth",
                     "launches_per_step": v["launches_per_step"], "share_of_step": v["ms_per_step"] / prof_total}
 
     # ---- CPU baseline: the oracle on a bounded sample of the same workload ----
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        cores = max(1, min(os.cpu_count() or 1, 4))
-        rate, dt = oracle_rate(frames[:cores], L, mb, cores)
+        cores = max(1, min(os.cpu_count() or 1, 8))
+        nf = min(len(frames), 8)
+        rate, dt = oracle_rate(frames[:nf], L, mb, cores)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{cores} cfg2 frames encode+decode, one thread per frame ({dt:.1f} s)"}
+               "sample": f"{nf} of the step's cfg2 frames encode+decode on {cores} threads, one frame per "
+                         f"task ({dt:.1f} s wall, ~{nf * 2.2:.0f} CPU-s)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": t_max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int8 x int8 -> int32 (integer-only)", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "frames_per_gpu_per_step": B, "global_batch": B * world,
-                   "lanes_per_gpu": S, "frames_per_launch": B // S,
-                   "points_per_frame": npts / B, "voxels_per_frame": nvox / B, "parallelism": f"frames/dp{world}",
-                   "l2": "flushed between steps (256 MiB write, outside the events)"},
+        "config": run_config(B, world),
+        "details": {"lanes_per_gpu": S, "frames_per_launch": B // S, "points_per_frame": npts / B,
+                    "voxels_per_frame": nvox / B},
         "enc_fps": enc_fps, "dec_fps": dec_fps, "points_per_s": pts_tot / (t_max_ms / 1e3),
         "bpp": 8.0 * nbytes / npts, "bits_per_voxel": 8.0 * nbytes / nvox,
         "parity_sample_frame0": parity, "wall_s_timed_region": t_wall,

@@ -14,7 +14,7 @@ for r in rows[1:]:
     name = re.sub(r"\(.*", "", r[ki]).replace("void ", "").replace("pcc::<unnamed>::", "").replace("(anonymous namespace)::", "")
     name = re.sub(r"^.*::", "", name)
     v = float(r[vi].replace(",", ""))
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
     tot[name] += v * scale
     cnt[name] += 1
 T = sum(tot.values())

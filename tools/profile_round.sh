@@ -1,22 +1,21 @@
 #!/bin/bash
-# Round evidence: GPU tests, full default bench (JSON line), ncu launch list of one bench
-# step, and ncu --set full captures of the dominant kernels (1 GPU).
+# Round evidence on one GPU: parity tests, the default bench line (+ the reference arm),
+# the ncu launch list of one B=256 step, and ncu --set full of the longest launch of each
+# hot kernel.  Outputs land in gpurun_out/; tools/summarize_round.py turns them into profiles/.
 cd "$(dirname "$0")/.."
 python paper_2603_25260_b200/build.py > /dev/null || exit 1
 timeout -s KILL 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
 echo "gpu tests: $(tail -1 gpurun_out/pytest_gpu.log)"
 timeout -s KILL 900 python bench.py > gpurun_out/bench_default.log 2>&1
-tail -c 3000 gpurun_out/bench_default.log
-# launch list of one timed step (skip the 3 warm-up steps' launches)
-timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 239 -c 239 --csv \
-  --log-file gpurun_out/launches.csv python tools/step_once.py --batch 256 \
-  > gpurun_out/ncu_launches.log 2>&1
+tail -c 400 gpurun_out/bench_default.log
+timeout -s KILL 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_reference.log 2>&1
+tail -c 300 gpurun_out/bench_reference.log
+# launch list of one whole step (single codec instance, B = 256)
+timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches.csv python tools/step_once.py --batch 256 --steps 0 > gpurun_out/ncu_launches.log 2>&1
 echo "launch list: $(wc -l < gpurun_out/launches.csv) lines"
-# full captures: decoder predictor at level 11 and the largest conv / up / rans_dec launches
-timeout -s KILL 900 ncu --set full --import-source on --clock-control none -k regex:k_head_tc -s 15 -c 1 \
-  -o gpurun_out/full_head python tools/step_once.py --batch 256 > gpurun_out/ncu_full_head.log 2>&1
-timeout -s KILL 900 ncu --set full --import-source on --clock-control none -k regex:k_rans_dec -s 15 -c 1 \
-  -o gpurun_out/full_rdec python tools/step_once.py --batch 256 > gpurun_out/ncu_full_rdec.log 2>&1
-timeout -s KILL 900 ncu --set full --import-source on --clock-control none -k regex:k_conv3_tc -s 8 -c 2 \
-  -o gpurun_out/full_conv python tools/step_once.py --batch 256 > gpurun_out/ncu_full_conv.log 2>&1
+for k in "k_head_tc<.int.32, .int.32, .int.1:head_dec" "k_head_tc<.int.32, .int.32, .int.0:head_enc" \
+         "k_rans_dec:rans_dec" "k_conv3_tc:conv" "k_up_tc:up" "k_down_tc:down" "k_rs_scatter:sort_scatter"; do
+  bash tools/ncu_biggest.sh "${k%%:*}" "full_${k##*:}"
+done
 ls -la gpurun_out/*.ncu-rep
