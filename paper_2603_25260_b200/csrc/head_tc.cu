@@ -24,6 +24,7 @@ namespace {
 
 constexpr int TILE = 128;
 constexpr uint32_t IDESC = tc::idesc_i8(128, 256);
+constexpr int STG = 264;  // staged cdf row stride in u16 (528 B: 16-B aligned, STS.128/LDS.128 conflict-free)
 
 __device__ __forceinline__ int32_t lq8(int32_t z, RQ q) {  // Q8 logit, clamp +-2^24
   int64_t v = int64_t(z) * int64_t(q.mp);
@@ -66,7 +67,8 @@ struct SmemLayout {
   static constexpr int THOLD = MBAR + 8;
   static constexpr int RED = MBAR + 16;          // [4][128] x (a, b) int32 = 4 KB
   static constexpr int ROWI = RED + 4096;        // [128] x 8 int32 = 4 KB
-  static constexpr int MASK = ROWI + 4096;       // decoder: [9][4] u32 leftover masks
+  static constexpr int STAGE = ROWI + 4096;      // decoder: 128 x STG u16 (66 KB)
+  static constexpr int MASK = STAGE + TILE * STG * 2;  // decoder: [9][4] u32 leftover masks
   static constexpr int END = MASK + 9 * 16;
 };
 
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   uint32_t* thold = reinterpret_cast<uint32_t*>(sm + S::THOLD);
   int32_t* red = reinterpret_cast<int32_t*>(sm + S::RED);    // red[(q*128 + r)*2 + {0,1}]
   int32_t* rowi = reinterpret_cast<int32_t*>(sm + S::ROWI);  // rowi[r*8 + k]
+  uint16_t* stage = reinterpret_cast<uint16_t*>(sm + S::STAGE);
   const int tid = threadIdx.x, warp = tid >> 5;
   const int r = 32 * (warp & 3) + (tid & 31);  // row of the tile (= TMEM lane)
   const int q = warp >> 2;                     // column quarter
@@ -341,60 +344,65 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         cf[row] = cm | (f << 16);
       }
     } else {
-      // pass 3a: p (padding column 255 -> 0) back into TMEM, quarter totals
-      uint32_t tq = 0;
+      uint16_t* srow = stage + r * STG;
+      uint32_t run = 0;
 #pragma unroll 1
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t v[16];
         tmem_ld16(taddr + ch * 16, v);
         tc::tmem_wait_ld();
         pchunk(v);
-        if (q == 3 && ch == 3) v[15] = 0u;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) tq += v[k];
-        tmem_st16(taddr + ch * 16, v);
-      }
-      __syncthreads();  // Ssum / istar reads of red done
-      red[(q * TILE + r) * 2] = int32_t(tq);
-      __syncthreads();
-      uint32_t off = 0, T = 0;
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        const uint32_t tqq = uint32_t(red[(qq * TILE + r) * 2]);
-        off += qq < q ? tqq : 0u;
-        T += tqq;
-      }
-      const uint32_t leftw = (65536u - T) * 0x10001u;
-      tmem_wait_st();
-      // pass 3b: the cumulative row = quarter offset + running sum, the leftover added to
-      // the elements after the first argmax (t = how many of a 8-element chunk are <=
-      // istar selects the half-word masks), straight to global in 16-byte stores (each
-      // thread writes its 128 contiguous bytes of the row; every cdf value below index
-      // 255 is < 2^16, so the packed adds never carry across halves)
-      const uint4* mask4 = reinterpret_cast<const uint4*>(sm + S::MASK);
-      uint4* dst = reinterpret_cast<uint4*>(cdf + size_t(valid ? row : 0u) * 256 + 64 * q);
-      uint32_t run = off;
-#pragma unroll 1
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t v[16];
-        tmem_ld16(taddr + ch * 16, v);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int k8 = 0; k8 < 16; k8 += 8) {
-          const int i0 = 64 * q + 16 * ch + k8;
-          const uint4 m = mask4[min(max(istar + 1 - i0, 0), 8)];
+        for (int k8 = 0; k8 < 16; k8 += 8) {  // 8 entries -> one 16-byte shared store
           uint32_t w[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const uint32_t c0 = run;
+            const uint32_t c0 = run;  // quarter-local prefix (< 2^16)
             run += v[k8 + 2 * u];
-            w[u] = __byte_perm(c0, run, 0x5410);
+            w[u] = (c0 & 0xffffu) | (run << 16);
             run += v[k8 + 2 * u + 1];
           }
-          w[0] += leftw & m.x, w[1] += leftw & m.y, w[2] += leftw & m.z, w[3] += leftw & m.w;
-          if (q == 3 && ch == 3 && k8 == 8) w[3] = (w[3] & 0xffffu) | 0xffff0000u;  // index 255: padding
-          if (valid) dst[2 * ch + (k8 >> 3)] = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint4*>(srow + 64 * q + ch * 16 + k8) = make_uint4(w[0], w[1], w[2], w[3]);
         }
+      }
+      if (q == 3) run -= 1u;  // padding column 255
+      __syncthreads();  // Ssum reads done
+      red[(q * TILE + r) * 2] = int32_t(run);
+      __syncthreads();
+      if (q == 0) {
+        uint32_t o = 0;
+        for (int qq = 0; qq < 4; ++qq) {
+          rowi[r * 8 + qq] = int32_t(o);  // prefix of the quarter totals
+          o += uint32_t(red[(qq * TILE + r) * 2]);
+        }
+        rowi[r * 8 + 4] = int32_t(65536u - o);  // leftover
+        rowi[r * 8 + 5] = istar;
+      }
+      __syncthreads();
+      // coalesced write-out: 16 rows per iteration, 32 threads x 16 bytes per 512-byte row.
+      // Packed u16 pairs: every cdf value below index 255 is < 2^16, so the quarter offset
+      // and the leftover are added to both halves at once without carries; the leftover
+      // goes to the elements after the first argmax: t = how many of the chunk's 8
+      // elements are <= istar selects the half-word mask of each word.
+      const uint32_t rows_here = (n - tile * TILE) < uint32_t(TILE) ? (n - tile * TILE) : uint32_t(TILE);
+      const uint32_t j = uint32_t(tid) & 31u, sub = uint32_t(tid) >> 5, jq = j >> 3;
+      const uint4* mask4 = reinterpret_cast<const uint4*>(sm + S::MASK);
+      const uint16_t* sp = stage + sub * STG + 8 * j;
+      const int32_t* rp = rowi + sub * 8;
+      uint4* gp = reinterpret_cast<uint4*>(cdf + (size_t(tile) * TILE + sub) * 256) + j;
+      for (uint32_t rr = sub; rr < rows_here; rr += 16, sp += 16 * STG, rp += 16 * 8, gp += 16 * 32) {
+        const uint32_t offw = uint32_t(rp[jq]) * 0x10001u;
+        const int2 li = *reinterpret_cast<const int2*>(rp + 4);  // leftover, first argmax
+        const uint32_t leftw = uint32_t(li.x) * 0x10001u;
+        const uint4 m = mask4[min(max(li.y + 1 - int(8 * j), 0), 8)];
+        const uint4 g = *reinterpret_cast<const uint4*>(sp);
+        uint4 o;
+        o.x = g.x + offw + (leftw & m.x);
+        o.y = g.y + offw + (leftw & m.y);
+        o.z = g.z + offw + (leftw & m.z);
+        o.w = g.w + offw + (leftw & m.w);
+        if (j == 31u) o.w = (o.w & 0xffffu) | 0xffff0000u;  // index 255: padding
+        *gp = o;
       }
     }
     tc::fence_before();
