@@ -69,7 +69,8 @@ struct SmemLayout {
   static constexpr int ROWI = RED + 4096;        // [128] x 8 int32 = 4 KB
   static constexpr int STAGE = ROWI + 4096;      // decoder: 128 x STG u16 (66 KB)
   static constexpr int MASK = STAGE + TILE * STG * 2;  // decoder: [9][4] u32 leftover masks
-  static constexpr int END = MASK + 9 * 16;
+  static constexpr int FST = MASK + 9 * 16;      // the tile's input rows F, prefetched by cp.async (<= 8 KB)
+  static constexpr int END = FST + TILE * 64;
 };
 
 // SAT = false when the model proves |z| can never reach the logit saturation thresholds
@@ -128,6 +129,26 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   const uint32_t ntiles = (n + TILE - 1) / TILE;
   uint32_t phase = 0;
 
+  // the next tile's feature rows are copied (cp.async) into smem while this tile runs
+  constexpr int CB = C < 16 ? C : 16, RCH = C / CB;  // copy chunk, chunks per row
+  auto prefetch_f = [&](uint32_t tl) {
+    if (tl < ntiles && tid < TILE * RCH) {
+      const int rr = tid / RCH, h = tid % RCH;
+      const uint32_t rw = tl * TILE + rr;
+      if (rw < n) {
+        if constexpr (CB == 16)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(sm + S::FST + rr * C + 16 * h)),
+                       "l"(F + size_t(rw) * C + 16 * h));
+        else
+          asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(tc::smem_u32(sm + S::FST + rr * C + CB * h)),
+                       "l"(F + size_t(rw) * C + CB * h), "n"(CB));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  prefetch_f(blockIdx.x);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint32_t row = tile * TILE + r;
     const bool valid = row < n;
@@ -135,7 +156,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     {
       int32_t fw[CW];
 #pragma unroll
-      for (int w = 0; w < CW; ++w) fw[w] = valid ? reinterpret_cast<const int32_t*>(F + size_t(row) * C)[w] : 0;
+      for (int w = 0; w < CW; ++w) fw[w] = valid ? reinterpret_cast<const int32_t*>(sm + S::FST + r * C)[w] : 0;
       uint32_t ab[2] = {0u, 0u};
       int32_t hacc[HQ];
 #pragma unroll
@@ -186,6 +207,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       tc::mma_i8(tbase, adesc, bdesc, IDESC, 1u);
       tc::commit(mbar);
     }
+    prefetch_f(tile + gridDim.x);  // every thread has read its F row (barrier above)
     tc::mbar_wait(mbar, phase);
     phase ^= 1u;
     tc::fence_after();
@@ -405,8 +427,9 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         *gp = o;
       }
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     tc::fence_before();
-    __syncthreads();  // TMEM / sA / stage / red reused by the next tile
+    __syncthreads();  // TMEM / sA / stage / red reused by the next tile; next F rows landed
     tc::fence_after();
   }
   __syncthreads();
