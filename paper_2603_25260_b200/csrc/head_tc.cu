@@ -99,6 +99,9 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   const int tid = threadIdx.x, warp = tid >> 5;
   const int r = 32 * (warp & 3) + (tid & 31);  // row of the tile (= TMEM lane)
   const int q = warp >> 2;                     // column quarter
+  // the 4 threads of a row are the 4 warps with the same warp % 4: row exchanges (red,
+  // rowi, the staged cdf rows) synchronise only those 128 threads (named barrier 1 + w%4)
+  auto bar_rows = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + (warp & 3)) : "memory"); };
   constexpr int CW = C / 4, HW = H / 4, HQ = H / 4;  // HQ hidden units per thread
 
   for (int k = tid; k < 256 * 8; k += NT) {
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     }
     red[(q * TILE + r) * 2] = zmax;
     red[(q * TILE + r) * 2 + 1] = zmin;
-    __syncthreads();
+    bar_rows();
     const int32_t zmx = max(max(red[r * 2], red[(TILE + r) * 2]), max(red[(2 * TILE + r) * 2], red[(3 * TILE + r) * 2]));
     const int32_t zmn =
         min(min(red[r * 2 + 1], red[(TILE + r) * 2 + 1]), min(red[(2 * TILE + r) * 2 + 1], red[(3 * TILE + r) * 2 + 1]));
@@ -285,10 +288,10 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       tmem_st16(taddr + ch * 16, v);
     }
     const int ist = int(kmin < 256u ? kmin : (1u << 30));
-    __syncthreads();  // everyone has read red (pass-1 values) before it is overwritten
+    bar_rows();  // everyone has read red (pass-1 values) before it is overwritten
     red[(q * TILE + r) * 2] = int32_t(ssum);
     red[(q * TILE + r) * 2 + 1] = ist;
-    __syncthreads();
+    bar_rows();
     const uint32_t Ssum = uint32_t(red[r * 2]) + uint32_t(red[(TILE + r) * 2]) + uint32_t(red[(2 * TILE + r) * 2]) +
                           uint32_t(red[(3 * TILE + r) * 2]);
     const int istar = min(min(red[r * 2 + 1], red[(TILE + r) * 2 + 1]),
@@ -348,11 +351,11 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         }
       }
       if (q == 3) tot -= 1u;  // the padding column 255 (e = 0 -> p = 1) is not a symbol
-      __syncthreads();  // Ssum reads done
+      bar_rows();  // Ssum reads done
       red[(q * TILE + r) * 2] = int32_t(tot);
       rowi[r * 8 + q] = int32_t(cum);
       rowi[r * 8 + 4 + q] = int32_t(fq);
-      __syncthreads();
+      bar_rows();
       if (q == 0 && valid) {
         uint32_t T = 0, cm = 0, f = 0;
         for (int qq = 0; qq < 4; ++qq) {
@@ -388,9 +391,9 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         }
       }
       if (q == 3) run -= 1u;  // padding column 255
-      __syncthreads();  // Ssum reads done
+      bar_rows();  // Ssum reads done
       red[(q * TILE + r) * 2] = int32_t(run);
-      __syncthreads();
+      bar_rows();
       if (q == 0) {
         uint32_t o = 0;
         for (int qq = 0; qq < 4; ++qq) {
@@ -400,19 +403,22 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         rowi[r * 8 + 4] = int32_t(65536u - o);  // leftover
         rowi[r * 8 + 5] = istar;
       }
-      __syncthreads();
+      bar_rows();
       // coalesced write-out: 16 rows per iteration, 32 threads x 16 bytes per 512-byte row.
       // Packed u16 pairs: every cdf value below index 255 is < 2^16, so the quarter offset
       // and the leftover are added to both halves at once without carries; the leftover
       // goes to the elements after the first argmax: t = how many of the chunk's 8
       // elements are <= istar selects the half-word mask of each word.
       const uint32_t rows_here = (n - tile * TILE) < uint32_t(TILE) ? (n - tile * TILE) : uint32_t(TILE);
-      const uint32_t j = uint32_t(tid) & 31u, sub = uint32_t(tid) >> 5, jq = j >> 3;
+      // rows of this warp's lane quarter only (32 * (w % 4) + w / 4 + 4 i): staged by the
+      // same 128 threads, so the row barrier suffices
+      const uint32_t j = uint32_t(tid) & 31u, sub = 32u * uint32_t(warp & 3) + uint32_t(warp >> 2), jq = j >> 3;
       const uint4* mask4 = reinterpret_cast<const uint4*>(sm + S::MASK);
       const uint16_t* sp = stage + sub * STG + 8 * j;
       const int32_t* rp = rowi + sub * 8;
       uint4* gp = reinterpret_cast<uint4*>(cdf + (size_t(tile) * TILE + sub) * 256) + j;
-      for (uint32_t rr = sub; rr < rows_here; rr += 16, sp += 16 * STG, rp += 16 * 8, gp += 16 * 32) {
+      const uint32_t rend = min(rows_here, 32u * uint32_t(warp & 3) + 32u);
+      for (uint32_t rr = sub; rr < rend; rr += 4, sp += 4 * STG, rp += 4 * 8, gp += 4 * 32) {
         const uint32_t offw = uint32_t(rp[jq]) * 0x10001u;
         const int2 li = *reinterpret_cast<const int2*>(rp + 4);  // leftover, first argmax
         const uint32_t leftw = uint32_t(li.x) * 0x10001u;
