@@ -288,7 +288,6 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       tmem_st16(taddr + ch * 16, v);
     }
     const int ist = int(kmin < 256u ? kmin : (1u << 30));
-    if (MODE == 1 && q == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // staging free
     bar_rows();  // everyone has read red (pass-1 values) before it is overwritten
     red[(q * TILE + r) * 2] = int32_t(ssum);
     red[(q * TILE + r) * 2 + 1] = ist;
@@ -395,38 +394,43 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       bar_rows();  // Ssum reads done
       red[(q * TILE + r) * 2] = int32_t(run);
       bar_rows();
-      // every thread finishes its own staged quarter: + the quarter offset, + the leftover
-      // on the elements after the first argmax (t = how many of an 8-element chunk are <=
-      // istar selects the half-word masks).  Packed u16 pairs: every cdf value below index
-      // 255 is < 2^16, so both halves are added at once without carries.
-      uint32_t off = 0, T = 0;
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        const uint32_t tqq = uint32_t(red[(qq * TILE + r) * 2]);
-        off += qq < q ? tqq : 0u;
-        T += tqq;
+      if (q == 0) {
+        uint32_t o = 0;
+        for (int qq = 0; qq < 4; ++qq) {
+          rowi[r * 8 + qq] = int32_t(o);  // prefix of the quarter totals
+          o += uint32_t(red[(qq * TILE + r) * 2]);
+        }
+        rowi[r * 8 + 4] = int32_t(65536u - o);  // leftover
+        rowi[r * 8 + 5] = istar;
       }
-      const uint32_t offw = off * 0x10001u, leftw = (65536u - T) * 0x10001u;
-      const uint4* mask4 = reinterpret_cast<const uint4*>(sm + S::MASK);
-      uint4* sq = reinterpret_cast<uint4*>(srow + 64 * q);
-#pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
-        const uint4 m = mask4[min(max(istar + 1 - (64 * q + 8 * c8), 0), 8)];
-        uint4 g = sq[c8];
-        g.x += offw + (leftw & m.x);
-        g.y += offw + (leftw & m.y);
-        g.z += offw + (leftw & m.z);
-        g.w += offw + (leftw & m.w);
-        if (c8 == 7 && q == 3) g.w = (g.w & 0xffffu) | 0xffff0000u;  // index 255: padding
-        sq[c8] = g;
-      }
-      tc::fence_async_smem();  // the staged row is read by the bulk copy (async proxy)
       bar_rows();
-      if (q == 0 && valid) {  // the finished 512-byte row -> global with one bulk copy
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;\n"
-                     "cp.async.bulk.commit_group;\n" ::"l"(cdf + size_t(row) * 256),
-                     "r"(tc::smem_u32(srow))
-                     : "memory");
+      // coalesced write-out: 16 rows per iteration, 32 threads x 16 bytes per 512-byte row.
+      // Packed u16 pairs: every cdf value below index 255 is < 2^16, so the quarter offset
+      // and the leftover are added to both halves at once without carries; the leftover
+      // goes to the elements after the first argmax: t = how many of the chunk's 8
+      // elements are <= istar selects the half-word mask of each word.
+      const uint32_t rows_here = (n - tile * TILE) < uint32_t(TILE) ? (n - tile * TILE) : uint32_t(TILE);
+      // rows of this warp's lane quarter only (32 * (w % 4) + w / 4 + 4 i): staged by the
+      // same 128 threads, so the row barrier suffices
+      const uint32_t j = uint32_t(tid) & 31u, sub = 32u * uint32_t(warp & 3) + uint32_t(warp >> 2), jq = j >> 3;
+      const uint4* mask4 = reinterpret_cast<const uint4*>(sm + S::MASK);
+      const uint16_t* sp = stage + sub * STG + 8 * j;
+      const int32_t* rp = rowi + sub * 8;
+      uint4* gp = reinterpret_cast<uint4*>(cdf + (size_t(tile) * TILE + sub) * 256) + j;
+      const uint32_t rend = min(rows_here, 32u * uint32_t(warp & 3) + 32u);
+      for (uint32_t rr = sub; rr < rend; rr += 4, sp += 4 * STG, rp += 4 * 8, gp += 4 * 32) {
+        const uint32_t offw = uint32_t(rp[jq]) * 0x10001u;
+        const int2 li = *reinterpret_cast<const int2*>(rp + 4);  // leftover, first argmax
+        const uint32_t leftw = uint32_t(li.x) * 0x10001u;
+        const uint4 m = mask4[min(max(li.y + 1 - int(8 * j), 0), 8)];
+        const uint4 g = *reinterpret_cast<const uint4*>(sp);
+        uint4 o;
+        o.x = g.x + offw + (leftw & m.x);
+        o.y = g.y + offw + (leftw & m.y);
+        o.z = g.z + offw + (leftw & m.z);
+        o.w = g.w + offw + (leftw & m.w);
+        if (j == 31u) o.w = (o.w & 0xffffu) | 0xffff0000u;  // index 255: padding
+        *gp = o;
       }
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -434,7 +438,6 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     __syncthreads();  // TMEM / sA / stage / red reused by the next tile; next F rows landed
     tc::fence_after();
   }
-  if (MODE == 1) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<256>(tbase);
 }
