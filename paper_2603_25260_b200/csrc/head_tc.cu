@@ -22,6 +22,24 @@ namespace pcc {
 
 namespace {
 
+#ifdef PCC_TRACE
+// development-only phase timer (tools/micro/trace_head.py): cycles per phase, summed over
+// the CTAs' thread 0 (row 0, quarter 0) and thread 480 (row 96, quarter 3)
+__device__ unsigned long long g_head_trace[2][8];
+#define HEAD_TRACE(slot, t0)                                                          \
+  do {                                                                                \
+    if ((threadIdx.x & 0x1df) == 0) {                                                 \
+      const long long t1_ = clock64();                                                \
+      atomicAdd(&g_head_trace[MODE][slot], (unsigned long long)(t1_ - (t0)));         \
+      (t0) = t1_;                                                                     \
+    }                                                                                 \
+  } while (0)
+#else
+#define HEAD_TRACE(slot, t0) \
+  do {                       \
+  } while (0)
+#endif
+
 constexpr int TILE = 128;
 constexpr uint32_t IDESC = tc::idesc_i8(128, 256);
 constexpr int STG = 264;  // staged cdf row stride in u16 (528 B: 16-B aligned, STS.128/LDS.128 conflict-free)
@@ -132,65 +150,59 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   const uint32_t ntiles = (n + TILE - 1) / TILE;
   uint32_t phase = 0;
 
-  // the next tile's feature rows are copied (cp.async) into smem while this tile runs
+  // The next tile's feature rows are copied (cp.async) into smem while this tile runs;
+  // row r's chunks are copied by the row's own quarter threads q < RCH, so a row barrier
+  // makes them visible to the row's 4 threads.
   constexpr int CB = C < 16 ? C : 16, RCH = C / CB;  // copy chunk, chunks per row
   auto prefetch_f = [&](uint32_t tl) {
-    if (tl < ntiles && tid < TILE * RCH) {
-      const int rr = tid / RCH, h = tid % RCH;
-      const uint32_t rw = tl * TILE + rr;
-      if (rw < n) {
-        if constexpr (CB == 16)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(sm + S::FST + rr * C + 16 * h)),
-                       "l"(F + size_t(rw) * C + 16 * h));
-        else
-          asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(tc::smem_u32(sm + S::FST + rr * C + CB * h)),
-                       "l"(F + size_t(rw) * C + CB * h), "n"(CB));
-      }
+    const uint32_t rw = tl * TILE + r;
+    if (tl < ntiles && q < RCH && rw < n) {
+      if constexpr (CB == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(sm + S::FST + r * C + 16 * q)),
+                     "l"(F + size_t(rw) * C + 16 * q));
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(tc::smem_u32(sm + S::FST + r * C + CB * q)),
+                     "l"(F + size_t(rw) * C + CB * q), "n"(CB));
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  prefetch_f(blockIdx.x);
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  __syncthreads();
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t row = tile * TILE + r;
-    const bool valid = row < n;
-    // ---- hidden layer: this thread's H/4 units of row r, into the A operand ----
-    {
-      int32_t fw[CW];
+  // hidden layer of tile tl: this thread's H/4 units of row r, into the A operand; then the
+  // logit bias b2 initialises the accumulator (columns 64q.. of row r): the MMA adds a W2^T
+  // onto it, so the passes read z = b2 + a W2^T directly
+  auto hidden_and_bias = [&](uint32_t tl) {
+    const uint32_t rw = tl * TILE + r;
+    const bool vr = rw < n;
+    int32_t fw[CW];
 #pragma unroll
-      for (int w = 0; w < CW; ++w) fw[w] = valid ? reinterpret_cast<const int32_t*>(sm + S::FST + r * C)[w] : 0;
-      uint32_t ab[2] = {0u, 0u};
-      int32_t hacc[HQ];
+    for (int w = 0; w < CW; ++w) fw[w] = vr ? reinterpret_cast<const int32_t*>(sm + S::FST + r * C)[w] : 0;
+    uint32_t ab[2] = {0u, 0u};
+    int32_t hacc[HQ];
 #pragma unroll
-      for (int hh = 0; hh < HQ; ++hh) {
-        const int h = q * HQ + hh;
-        int32_t acc = sb1[h];
+    for (int hh = 0; hh < HQ; ++hh) {
+      const int h = q * HQ + hh;
+      int32_t acc = sb1[h];
 #pragma unroll
-        for (int w = 0; w < CW; ++w) acc = __dp4a(fw[w], sW1[h * CW + w], acc);
-        hacc[hh] = acc;
-      }
-      if (HQ % 4 == 0 && rq1.fast_s) {
-#pragma unroll
-        for (int g4 = 0; g4 < HQ / 4; ++g4)
-          ab[g4] = pack_sat4(rq_s(hacc[4 * g4], rq1), rq_s(hacc[4 * g4 + 1], rq1), rq_s(hacc[4 * g4 + 2], rq1),
-                             rq_s(hacc[4 * g4 + 3], rq1));
-      } else {
-#pragma unroll
-        for (int hh = 0; hh < HQ; ++hh) ab[hh >> 2] |= (uint32_t(rq8(hacc[hh], rq1)) & 0xffu) << (8 * (hh & 3));
-      }
-      uint8_t* dst = sA + tc::kmaj_off(r, q * HQ);
-      if constexpr (HQ == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(ab[0], ab[1]);
-      else if constexpr (HQ == 4) *reinterpret_cast<uint32_t*>(dst) = ab[0];
-      else *reinterpret_cast<uint16_t*>(dst) = uint16_t(ab[0]);
-      if (a_dbg && valid) {
-        int8_t* ad = a_dbg + size_t(row) * H + q * HQ;
-#pragma unroll
-        for (int hh = 0; hh < HQ; ++hh) ad[hh] = int8_t(ab[hh >> 2] >> (8 * (hh & 3)));
-      }
+      for (int w = 0; w < CW; ++w) acc = __dp4a(fw[w], sW1[h * CW + w], acc);
+      hacc[hh] = acc;
     }
-    // the logit bias b2 initialises the accumulator (columns 64q.. of row r): the MMA adds
-    // a W2^T onto it, so the passes below read z = b2 + a W2^T directly
+    if (HQ % 4 == 0 && rq1.fast_s) {
+#pragma unroll
+      for (int g4 = 0; g4 < HQ / 4; ++g4)
+        ab[g4] = pack_sat4(rq_s(hacc[4 * g4], rq1), rq_s(hacc[4 * g4 + 1], rq1), rq_s(hacc[4 * g4 + 2], rq1),
+                           rq_s(hacc[4 * g4 + 3], rq1));
+    } else {
+#pragma unroll
+      for (int hh = 0; hh < HQ; ++hh) ab[hh >> 2] |= (uint32_t(rq8(hacc[hh], rq1)) & 0xffu) << (8 * (hh & 3));
+    }
+    uint8_t* dst = sA + tc::kmaj_off(r, q * HQ);
+    if constexpr (HQ == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(ab[0], ab[1]);
+    else if constexpr (HQ == 4) *reinterpret_cast<uint32_t*>(dst) = ab[0];
+    else *reinterpret_cast<uint16_t*>(dst) = uint16_t(ab[0]);
+    if (a_dbg && vr) {
+      int8_t* ad = a_dbg + size_t(rw) * H + q * HQ;
+#pragma unroll
+      for (int hh = 0; hh < HQ; ++hh) ad[hh] = int8_t(ab[hh >> 2] >> (8 * (hh & 3)));
+    }
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch) {
       uint32_t bv[16];
@@ -202,18 +214,33 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       tmem_st16(taddr + ch * 16, bv);
     }
     tmem_wait_st();
-    tc::fence_async_smem();
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
+  };
+  if (blockIdx.x < ntiles) {
+    prefetch_f(blockIdx.x);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    bar_rows();
+    hidden_and_bias(blockIdx.x);
+  }
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  long long tr0 = clock64();
+  (void)tr0;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t row = tile * TILE + r;
+    const bool valid = row < n;
+    // A operand and bias-initialised accumulator of this tile are complete (end of the
+    // previous iteration / prologue)
     if (tid == 0) {
       tc::mma_i8(tbase, adesc, bdesc, IDESC, 1u);
       tc::commit(mbar);
     }
-    prefetch_f(tile + gridDim.x);  // every thread has read its F row (barrier above)
+    prefetch_f(tile + gridDim.x);  // the previous F rows were consumed before the barrier
     tc::mbar_wait(mbar, phase);
     phase ^= 1u;
     tc::fence_after();
+    HEAD_TRACE(1, tr0);
 
     // ---- pass 1: max of z (the requant is monotone non-decreasing, m >= 0, so
     //      max_i lq(z_i) = lq(max_i z_i)) ----
@@ -241,6 +268,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     const int32_t mu = lq8(zmx, rql);
     // the whole row avoids saturation: l = low word of the 64-bit shift, no selects
     const bool nosat = !SAT || (zmx <= zsat_hi && zmn >= zsat_lo);
+    HEAD_TRACE(2, tr0);
     // ---- pass 2: Q8 logit, e = LUT[delta >> 2] (0 beyond 16 nats), local sum and
     //      local first index with delta == 0 (e stored back into TMEM) ----
     uint32_t ssum = 0;
@@ -297,6 +325,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     const int istar = min(min(red[r * 2 + 1], red[(TILE + r) * 2 + 1]),
                           min(red[(2 * TILE + r) * 2 + 1], red[(3 * TILE + r) * 2 + 1]));
     tmem_wait_st();
+    HEAD_TRACE(3, tr0);
     // ---- pass 3: p = 1 + floor(e * 65281 / S) (exact), leftover to the first argmax ----
     // q = floor(e * 65281 / S): estimate with the 32-bit reciprocal inv32 =
     // floor(65281 * 2^32 / S) (< 2^24 since S >= LUT[0] = 2^24), q_est in {q - 1, q},
@@ -351,6 +380,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         }
       }
       if (q == 3) tot -= 1u;  // the padding column 255 (e = 0 -> p = 1) is not a symbol
+      HEAD_TRACE(4, tr0);
       bar_rows();  // Ssum reads done
       red[(q * TILE + r) * 2] = int32_t(tot);
       rowi[r * 8 + q] = int32_t(cum);
@@ -391,6 +421,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         }
       }
       if (q == 3) run -= 1u;  // padding column 255
+      HEAD_TRACE(4, tr0);
       bar_rows();  // Ssum reads done
       red[(q * TILE + r) * 2] = int32_t(run);
       bar_rows();
@@ -433,9 +464,18 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         *gp = o;
       }
     }
+    HEAD_TRACE(5, tr0);
+    // next tile: its F rows landed (own copies + row barrier), hidden layer into A and the
+    // bias into this thread's TMEM columns (all of this tile's TMEM reads are done)
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    bar_rows();
+    if (tile + gridDim.x < ntiles) hidden_and_bias(tile + gridDim.x);
+    HEAD_TRACE(0, tr0);
+    tc::fence_async_smem();
     tc::fence_before();
-    __syncthreads();  // TMEM / sA / stage / red reused by the next tile; next F rows landed
+    __syncthreads();  // A operand + bias complete; stage / red / rowi reused by the next tile
+    tc::fence_after();
+    HEAD_TRACE(6, tr0);
     tc::fence_after();
   }
   __syncthreads();
@@ -532,3 +572,14 @@ void gemm_i8_test(pcc_ctx c, const int8_t* dA, const int8_t* dB, int N, int32_t*
 }
 
 }  // namespace pcc
+
+#ifdef PCC_TRACE
+extern "C" int pcc_trace_head(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, pcc::g_head_trace, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(pcc::g_head_trace, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
