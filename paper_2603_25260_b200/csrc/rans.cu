@@ -55,9 +55,10 @@ __device__ __forceinline__ uint32_t ld_u32(const uint8_t* p) {
 // do not depend on the rANS state, so they are prefetched DEC_STAGES steps ahead into
 // shared memory with TMA bulk copies; the renormalisation words are consumed in stream order
 // and are held in a 96-word register window (three words per lane) refilled 64 words
-// ahead, so no step waits on a dependent global load.
-constexpr int DEC_STAGES = 4;
-
+// ahead, so no step waits on a dependent global load.  DEC_STAGES (2..4) is chosen per
+// launch: the deepest prefetch whose smem footprint still fits every segment's CTA into
+// one wave (a second, partial wave of a bandwidth-bound level costs more than depth).
+template <int DEC_STAGES>
 __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs, int nseg, const uint8_t* __restrict__ bs,
                                                  const uint16_t* __restrict__ cdf, uint8_t* __restrict__ X,
                                                  uint32_t* __restrict__ err, int stage_rows) {
@@ -182,15 +183,27 @@ void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, c
                  uint32_t* err, int max_lanes) {
   if (nseg == 0) return;
   const int stage_rows = max_lanes <= 8 ? 8 : (max_lanes <= 16 ? 16 : 32);
-  const size_t smem = size_t(DEC_STAGES) * stage_rows * 256 * sizeof(uint16_t);
   static bool attr = false;
   if (!attr) {
-    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(DEC_STAGES * 32 * 256 * sizeof(uint16_t))));
+    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 32 * 512));
+    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32 * 512));
+    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 512));
     attr = true;
   }
+  // CTAs per SM that fit in 227 KB of shared memory (+1 KB reserved per CTA), at most 32
+  auto per_sm = [&](int st) { return std::min(32, int(232448 / (st * stage_rows * 512 + 1024 + 64))); };
+  int st = 4;
+  while (st > 2 && size_t(nseg) > size_t(per_sm(st)) * size_t(c->sm_count)) --st;
+  static const int forced = [] {
+    const char* e = getenv("PCC_DEC_STAGES");  // development override (2..4)
+    return e ? atoi(e) : 0;
+  }();
+  if (forced >= 2 && forced <= 4) st = forced;
+  const size_t smem = size_t(st) * stage_rows * 512;
   Prof p(c, "rans_dec", 0);
-  k_rans_dec<<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, X, err, stage_rows);
+  if (st == 4) k_rans_dec<4><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, X, err, stage_rows);
+  else if (st == 3) k_rans_dec<3><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, X, err, stage_rows);
+  else k_rans_dec<2><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, X, err, stage_rows);
   launched(c);
 }
 
