@@ -55,9 +55,8 @@ __device__ __forceinline__ uint32_t ld_u32(const uint8_t* p) {
 // do not depend on the rANS state, so they are prefetched DEC_STAGES steps ahead into
 // shared memory with TMA bulk copies; the renormalisation words are consumed in stream order
 // and are held in a 96-word register window (three words per lane) refilled 64 words
-// ahead, so no step waits on a dependent global load.  DEC_STAGES (2..4) is chosen per
-// launch: the deepest prefetch whose smem footprint still fits every segment's CTA into
-// one wave (a second, partial wave of a bandwidth-bound level costs more than depth).
+// ahead, so no step waits on a dependent global load.  DEC_STAGES = 2 by default (more
+// resident CTAs per SM beat deeper prefetch on the bandwidth-bound levels).
 template <int DEC_STAGES>
 __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs, int nseg, const uint8_t* __restrict__ bs,
                                                  const uint16_t* __restrict__ cdf, uint8_t* __restrict__ X,
@@ -190,10 +189,10 @@ void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, c
     PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 512));
     attr = true;
   }
-  // CTAs per SM that fit in 227 KB of shared memory (+1 KB reserved per CTA), at most 32
-  auto per_sm = [&](int st) { return std::min(32, int(232448 / (st * stage_rows * 512 + 1024 + 64))); };
-  int st = 4;
-  while (st > 2 && size_t(nseg) > size_t(per_sm(st)) * size_t(c->sm_count)) --st;
+  // two stages: measured best on the B = 256 bench (2.55 ms vs 2.87 / 3.02 ms per step for
+  // 3 / 4 stages): the decode is bandwidth-bound on the largest levels, where more CTAs
+  // resident per SM beat deeper prefetch
+  int st = 2;
   static const int forced = [] {
     const char* e = getenv("PCC_DEC_STAGES");  // development override (2..4)
     return e ? atoi(e) : 0;
