@@ -169,69 +169,94 @@ __global__ void __launch_bounds__(LV_T) k_lvl_count(const uint64_t* __restrict__
   }
 }
 
+// Node index of leaf i at depth d = #{j < i : lvl(j) <= d}.  Per block: all four rounds'
+// keys are loaded up front; phase A counts, per (round, warp, depth), the leaves that
+// start a node (one ballot per depth from the warp's minimum level); phase B turns the
+// counts into exclusive bases (one thread per depth); phase C recomputes the ranks and
+// writes each new node (key, child start = own index one depth down, parent = own index
+// one depth up (minus one when the node is the parent's continuation), occupancy bit into
+// the parent's code).
 __global__ void __launch_bounds__(LV_T) k_lvl_scatter(const uint64_t* __restrict__ keys, size_t n, int L, int B,
                                                       const uint32_t* __restrict__ off, uint32_t nblk,
                                                       uint64_t* __restrict__ key_all, uint8_t* __restrict__ code_all,
                                                       uint32_t* __restrict__ cs_all, uint32_t* __restrict__ par_all,
                                                       uint32_t* __restrict__ foff) {
-  __shared__ uint32_t wcnt[LV_W][MAX_DEPTH + 1];
-  __shared__ uint32_t run[MAX_DEPTH + 1];
+  __shared__ uint32_t wb[LV_R][LV_W][MAX_DEPTH + 2];  // counts, then exclusive local bases
   __shared__ uint32_t nbs[MAX_DEPTH + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x <= L) {
-    run[threadIdx.x] = off[size_t(threadIdx.x) * nblk + blockIdx.x];  // global index base (incl. nb[d])
-    nbs[threadIdx.x] = off[size_t(threadIdx.x) * nblk];                // nb[d]
-  }
   const unsigned lt = (1u << lane) - 1u;
+  uint64_t key[LV_R];
+  int lvl[LV_R];
+#pragma unroll
   for (int r = 0; r < LV_R; ++r) {
-    size_t i = size_t(blockIdx.x) * LV_TILE + size_t(r) * LV_T + threadIdx.x;
-    const bool valid = i < n;
-    const int lvl = valid ? leaf_lvl(keys, i, L) : L + 1;
-    const uint64_t key = valid ? keys[i] : 0ull;
-    uint32_t rk[MAX_DEPTH + 1];
-#pragma unroll
-    for (int d = 0; d <= MAX_DEPTH; ++d) {
-      if (d > L) break;
-      unsigned b = __ballot_sync(0xffffffffu, lvl <= d);
-      rk[d] = __popc(b & lt);
-      if (lane == 0) wcnt[w][d] = __popc(b);
-    }
-    __syncthreads();
-    // excl_d(i) = run[d] + sum of earlier warps + rank  (global index incl. nb[d])
-    uint32_t ex[MAX_DEPTH + 1];
-#pragma unroll
-    for (int d = 0; d <= MAX_DEPTH; ++d) {
-      if (d > L) break;
-      uint32_t s = run[d];
-      for (int ww = 0; ww < w; ++ww) s += wcnt[ww][d];
-      ex[d] = s + rk[d] - nbs[d];  // local index within depth d
-    }
-    if (valid && lvl <= L) {
-      const int f = (B > 1) ? int(key >> (3 * L)) : 0;
-#pragma unroll
-      for (int d = 0; d <= MAX_DEPTH; ++d) {
-        if (d > L) break;
-        if (d < lvl) continue;
-        const size_t g = size_t(nbs[d]) + ex[d];
-        key_all[g] = key >> (3 * (L - d));
-        if (d < L) cs_all[g] = ex[d + 1];
-        if (d >= 1) {
-          const uint32_t p = ex[d - 1] - (lvl == d ? 1u : 0u);
-          par_all[g] = p;
-          const size_t gp = size_t(nbs[d - 1]) + p;
-          const uint32_t bit = 1u << uint32_t((key >> (3 * (L - d))) & 7u);
-          atomicOr(reinterpret_cast<unsigned*>(code_all + (gp & ~size_t(3))), bit << (8 * (gp & 3)));
+    const size_t i = size_t(blockIdx.x) * LV_TILE + size_t(r) * LV_T + threadIdx.x;
+    key[r] = i < n ? keys[i] : 0ull;
+    const uint64_t pk = (i < n && i > 0) ? keys[i - 1] : 0ull;
+    int l = L + 1;
+    if (i < n) {
+      if (i == 0) l = 0;
+      else {
+        const uint64_t x = key[r] ^ pk;
+        if (x != 0) {
+          const int hb = 63 - __clzll((long long)x);
+          l = L - hb / 3;
+          l = l < 0 ? 0 : l;
         }
-        if (lvl == 0) foff[size_t(d) * (B + 1) + f] = ex[d];
       }
     }
-    __syncthreads();
-    if (threadIdx.x <= L) {
-      uint32_t s = 0;
-      for (int ww = 0; ww < LV_W; ++ww) s += wcnt[ww][threadIdx.x];
-      run[threadIdx.x] += s;
+    lvl[r] = l;
+  }
+  // phase A
+#pragma unroll
+  for (int r = 0; r < LV_R; ++r) {
+    const int dm = __reduce_min_sync(0xffffffffu, lvl[r]);
+    for (int d = 0; d <= L; ++d) {
+      const uint32_t cnt = d < dm ? 0u : uint32_t(__popc(__ballot_sync(0xffffffffu, lvl[r] <= d)));
+      if (lane == 0) wb[r][w][d] = cnt;
     }
-    __syncthreads();
+  }
+  if (threadIdx.x <= L) nbs[threadIdx.x] = off[size_t(threadIdx.x) * nblk];
+  __syncthreads();
+  // phase B
+  if (threadIdx.x <= L) {
+    const int d = threadIdx.x;
+    uint32_t sacc = off[size_t(d) * nblk + blockIdx.x] - off[size_t(d) * nblk];
+    for (int r = 0; r < LV_R; ++r)
+      for (int ww = 0; ww < LV_W; ++ww) {
+        const uint32_t cc = wb[r][ww][d];
+        wb[r][ww][d] = sacc;
+        sacc += cc;
+      }
+  }
+  __syncthreads();
+  // phase C
+#pragma unroll
+  for (int r = 0; r < LV_R; ++r) {
+    const int lv = lvl[r];
+    const int dm = __reduce_min_sync(0xffffffffu, lv);
+    if (dm > L) continue;  // warp of duplicates only
+    auto ex = [&](int d) -> uint32_t { return wb[r][w][d] + uint32_t(__popc(__ballot_sync(0xffffffffu, lv <= d) & lt)); };
+    const uint64_t k = key[r];
+    const int f = (B > 1) ? int(k >> (3 * L)) : 0;
+    uint32_t e_prev = dm >= 1 ? ex(dm - 1) : 0u, e_cur = ex(dm);
+    for (int d = dm; d <= L; ++d) {
+      const uint32_t e_next = d < L ? ex(d + 1) : 0u;
+      if (lv <= d) {
+        const size_t g = size_t(nbs[d]) + e_cur;
+        key_all[g] = k >> (3 * (L - d));
+        if (d < L) cs_all[g] = e_next;
+        if (d >= 1) {
+          const uint32_t p = e_prev - (lv == d ? 1u : 0u);
+          par_all[g] = p;
+          const size_t gp = size_t(nbs[d - 1]) + p;
+          const uint32_t bit = 1u << uint32_t((k >> (3 * (L - d))) & 7u);
+          atomicOr(reinterpret_cast<unsigned*>(code_all + (gp & ~size_t(3))), bit << (8 * (gp & 3)));
+        }
+        if (lv == 0) foff[size_t(d) * (B + 1) + f] = e_cur;
+      }
+      e_prev = e_cur;
+      e_cur = e_next;
+    }
   }
 }
 
