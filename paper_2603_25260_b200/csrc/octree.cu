@@ -56,85 +56,145 @@ __global__ void k_morton(const int32_t* __restrict__ xyz, size_t n, const uint64
 // ---- radix sort (LSD, 8-bit digits, stable per pass) ---------------------------------
 constexpr int RS_T = 256, RS_V = 16, RS_TILE = RS_T * RS_V, RS_W = RS_T / 32;
 
-__global__ void __launch_bounds__(RS_T) k_rs_hist(const uint64_t* __restrict__ keys, size_t n, int shift,
-                                                  uint32_t* __restrict__ hist, uint32_t ntiles) {
-  __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  size_t base = size_t(blockIdx.x) * RS_TILE;
-#pragma unroll 4
-  for (int k = 0; k < RS_V; ++k) {
-    size_t i = base + size_t(k) * RS_T + threadIdx.x;
-    uint32_t d = i < n ? uint32_t((keys[i] >> shift) & 255u) : 256u;
-    unsigned peers = __match_any_sync(0xffffffffu, d);
-    if (d < 256u && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[d], __popc(peers));
-  }
-  __syncthreads();
-  hist[size_t(threadIdx.x) * ntiles + blockIdx.x] = h[threadIdx.x];
+// ---- onesweep radix pass (decoupled look-back): one read + one write of the keys per
+// digit.  The global digit histograms of every pass come from one upfront read
+// (k_rs_ghist); each tile takes its id from an atomic counter (so every predecessor is
+// running), ranks its keys per digit (warp match_any, stable), publishes its
+// per-digit count (flag AGG), looks back over predecessors until an inclusive prefix
+// (flag INC) and publishes its own inclusive prefix, then scatters through smem.
+constexpr uint32_t OS_AGG = 1u << 30, OS_INC = 2u << 30, OS_CNT = (1u << 30) - 1u;
+constexpr int GH_MAXP = 8;  // passes covered by the global histogram (64-bit keys)
+
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
-__global__ void __launch_bounds__(RS_T) k_rs_scatter(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
-                                                     size_t n, int shift, const uint32_t* __restrict__ hscan,
-                                                     uint32_t ntiles) {
+// hist[p][d] += #keys with digit p == d, for p < npass (grid-stride, block-private smem
+// histograms, one global atomic per (block, pass, digit))
+__global__ void __launch_bounds__(256) k_rs_ghist(const uint64_t* __restrict__ keys, size_t n, int npass,
+                                                  uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[GH_MAXP][256];
+  for (int i = threadIdx.x; i < GH_MAXP * 256; i += 256) (&h[0][0])[i] = 0;
+  __syncthreads();
+  for (size_t i = size_t(blockIdx.x) * 256 + threadIdx.x; i < n; i += size_t(gridDim.x) * 256) {
+    const uint64_t k = keys[i];
+    for (int p = 0; p < npass; ++p) atomicAdd(&h[p][uint32_t(k >> (8 * p)) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npass * 256; i += 256) {
+    const uint32_t v = (&h[0][0])[i];
+    if (v) atomicAdd(&hist[i], v);
+  }
+}
+
+// hist[p][256] -> exclusive prefix over digits, in place (one warp per pass)
+__global__ void k_rs_gbase(uint32_t* __restrict__ hist, int npass) {
+  const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p >= npass) return;
+  uint32_t* h = hist + p * 256;
+  uint32_t v[8], s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += (v[k] = h[lane * 8 + k]);
+  uint32_t inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  uint32_t run = inc - s;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    h[lane * 8 + k] = run;
+    run += v[k];
+  }
+}
+
+__global__ void __launch_bounds__(RS_T) k_rs_onesweep(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                                      size_t n, int shift, const uint32_t* __restrict__ gbase,
+                                                      uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr) {
   __shared__ uint32_t wc[RS_W][257];
   __shared__ uint32_t tstart[256];
-  __shared__ uint32_t gbase[256];
+  __shared__ uint32_t gofs[256];
   __shared__ uint32_t wtot[RS_W];
+  __shared__ uint32_t s_tile;
   __shared__ uint64_t stage[RS_TILE];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   for (int i = threadIdx.x; i < RS_W * 257; i += RS_T) (&wc[0][0])[i] = 0;
   __syncthreads();
+  const uint32_t tile = s_tile;
   const unsigned lt = (1u << lane) - 1u;
   uint64_t kv[RS_V];
   uint32_t rk[RS_V];
-  const size_t wbase = size_t(blockIdx.x) * RS_TILE + size_t(w) * (RS_TILE / RS_W);
+  const size_t wbase = size_t(tile) * RS_TILE + size_t(w) * (RS_TILE / RS_W);
 #pragma unroll
   for (int t = 0; t < RS_V; ++t) {
-    size_t i = wbase + size_t(t) * 32 + lane;
-    uint64_t k = i < n ? in[i] : 0ull;
-    uint32_t d = i < n ? uint32_t((k >> shift) & 255u) : 256u;
-    unsigned peers = __match_any_sync(0xffffffffu, d);
-    uint32_t base = wc[w][d];
+    const size_t i = wbase + size_t(t) * 32 + lane;
+    const uint64_t k = i < n ? in[i] : 0ull;
+    const uint32_t d = i < n ? uint32_t((k >> shift) & 255u) : 256u;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t base = wc[w][d];
     __syncwarp();
     if (lane == __ffs(peers) - 1) wc[w][d] = base + __popc(peers);
     __syncwarp();
     kv[t] = k;
-    rk[t] = (d << 16) | (base + __popc(peers & lt));  // rank < 4096 fits 16 bits
+    rk[t] = (d << 16) | (base + __popc(peers & lt));
   }
   __syncthreads();
-  // per-digit exclusive prefix over warps; tile count per digit
+  const uint32_t d = threadIdx.x;  // one thread per digit from here
   uint32_t run = 0;
   for (int ww = 0; ww < RS_W; ++ww) {
-    uint32_t t = wc[ww][threadIdx.x];
-    wc[ww][threadIdx.x] = run;
+    const uint32_t t = wc[ww][d];
+    wc[ww][d] = run;
     run += t;
   }
-  // exclusive scan of run over the 256 digits (one per thread)
+  // publish this tile's count, look back for the exclusive prefix over earlier tiles
+  uint32_t* st = status + size_t(tile) * 256 + d;
+  uint32_t excl = 0;
+  if (tile == 0) {
+    st_release(st, OS_INC | run);
+  } else {
+    st_release(st, OS_AGG | run);
+    for (int64_t t = int64_t(tile) - 1; t >= 0;) {
+      const uint32_t v = ld_acquire(status + size_t(t) * 256 + d);
+      if ((v & ~OS_CNT) == 0u) continue;  // predecessor not published yet
+      excl += v & OS_CNT;
+      if (v & OS_INC) break;
+      --t;
+    }
+    st_release(st, OS_INC | (excl + run));
+  }
+  // exclusive scan of the tile's digit counts -> start of each digit in the staged tile
   uint32_t inc = run;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
     if (lane >= o) inc += t;
   }
   if (lane == 31) wtot[w] = inc;
   __syncthreads();
   uint32_t wpre = 0;
   for (int ww = 0; ww < w; ++ww) wpre += wtot[ww];
-  tstart[threadIdx.x] = wpre + inc - run;
-  gbase[threadIdx.x] = hscan[size_t(threadIdx.x) * ntiles + blockIdx.x];
+  tstart[d] = wpre + inc - run;
+  gofs[d] = gbase[d] + excl;
   __syncthreads();
 #pragma unroll
   for (int t = 0; t < RS_V; ++t) {
-    uint32_t d = rk[t] >> 16;
-    if (d < 256u) stage[tstart[d] + wc[w][d] + (rk[t] & 0xffffu)] = kv[t];
+    const uint32_t dd = rk[t] >> 16;
+    if (dd < 256u) stage[tstart[dd] + wc[w][dd] + (rk[t] & 0xffffu)] = kv[t];
   }
   __syncthreads();
-  const size_t tb = size_t(blockIdx.x) * RS_TILE;
+  const size_t tb = size_t(tile) * RS_TILE;
   const uint32_t nvalid = uint32_t((n - tb) < size_t(RS_TILE) ? (n - tb) : size_t(RS_TILE));
-  for (uint32_t p = threadIdx.x; p < nvalid; p += RS_T) {
-    uint64_t k = stage[p];
-    uint32_t d = uint32_t((k >> shift) & 255u);
-    out[gbase[d] + p - tstart[d]] = k;
+  for (uint32_t q = threadIdx.x; q < nvalid; q += RS_T) {
+    const uint64_t k = stage[q];
+    const uint32_t dd = uint32_t((k >> shift) & 255u);
+    out[gofs[dd] + q - tstart[dd]] = k;
   }
 }
 
@@ -332,19 +392,24 @@ void build_octree(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int B, in
   while ((1 << fb) < B) ++fb;
   const int bits = 3 * L + fb;
   const uint32_t ntiles = cdiv(n, RS_TILE);
-  uint32_t* hist = wsT<uint32_t>(c, "rs_hist", size_t(256) * ntiles + 1);
-  for (int sh = 0; sh < bits; sh += 8) {
-    {
-      Prof p(c, "sort", n * 8);
-      k_rs_hist<<<ntiles, RS_T, 0, s>>>(ka, n, sh, hist, ntiles);
-      launched(c);
-    }
-    scan_u32(c, hist, hist, size_t(256) * ntiles);
-    {
-      Prof p(c, "sort", n * 16);
-      k_rs_scatter<<<ntiles, RS_T, 0, s>>>(ka, kb, n, sh, hist, ntiles);
-      launched(c);
-    }
+  const int npass = (bits + 7) / 8;
+  // global digit histograms (one read), then one onesweep pass per digit
+  uint32_t* gh = wsT<uint32_t>(c, "rs_ghist", size_t(GH_MAXP) * 256 + GH_MAXP);
+  uint32_t* status = wsT<uint32_t>(c, "rs_status", size_t(npass) * ntiles * 256);
+  uint32_t* ctr = gh + size_t(GH_MAXP) * 256;
+  PCC_CUDA(cudaMemsetAsync(gh, 0, (size_t(GH_MAXP) * 256 + GH_MAXP) * sizeof(uint32_t), s));
+  PCC_CUDA(cudaMemsetAsync(status, 0, size_t(npass) * ntiles * 256 * sizeof(uint32_t), s));
+  {
+    Prof p(c, "sort", n * 8);
+    k_rs_ghist<<<std::min<unsigned>(ntiles, unsigned(c->sm_count) * 4u), 256, 0, s>>>(ka, n, npass, gh);
+    k_rs_gbase<<<1, 32 * GH_MAXP, 0, s>>>(gh, npass);
+    launched(c, 2);
+  }
+  for (int ps = 0; ps < npass; ++ps) {
+    Prof p(c, "sort", n * 16);
+    k_rs_onesweep<<<ntiles, RS_T, 0, s>>>(ka, kb, n, 8 * ps, gh + ps * 256, status + size_t(ps) * ntiles * 256,
+                                          ctr + ps);
+    launched(c);
     std::swap(ka, kb);
   }
   const uint64_t* sorted = ka;
