@@ -13,10 +13,6 @@
 //      (exact: 64-bit reciprocal + one integer correction) and either the (cum, freq)
 //      of the true symbol (encoder) or the cumulative row (decoder, staged in smem and
 //      written with coalesced stores).
-// MODE 2 (fused decoder): CTAs walk whole rANS segments (reading Q24)
-// instead of flat tiles.  A tile is floor(128 / K) * K consecutive symbols of one segment
-// (whole rANS steps), and once its cumulative rows are staged, warp 0 runs the tile's
-// rANS decode steps against them in shared memory, so the rows never reach HBM.
 // Bit-exact with the oracle's cdf_quantize / head_logits (integer arithmetic only).
 #include "pcc_internal.cuh"
 #include "rq.cuh"
@@ -29,7 +25,7 @@ namespace {
 #ifdef PCC_TRACE
 // development-only phase timer (tools/micro/trace_head.py): cycles per phase, summed over
 // the CTAs' thread 0 (row 0, quarter 0) and thread 480 (row 96, quarter 3)
-__device__ unsigned long long g_head_trace[3][8];
+__device__ unsigned long long g_head_trace[2][8];
 #define HEAD_TRACE(slot, t0)                                                          \
   do {                                                                                \
     if ((threadIdx.x & 0x1df) == 0) {                                                 \
@@ -92,172 +88,8 @@ struct SmemLayout {
   static constexpr int STAGE = ROWI + 4096;      // decoder: 128 x STG u16 (66 KB)
   static constexpr int MASK = STAGE + TILE * STG * 2;  // decoder: [9][4] u32 leftover masks
   static constexpr int FST = MASK + 9 * 16;      // the tile's input rows F, prefetched by cp.async (<= 8 KB)
-  static constexpr int DEC = FST + TILE * 64;    // MODE 2: rANS lane states [32] + segment scalars
-  static constexpr int END = DEC + 512;
+  static constexpr int END = FST + TILE * 64;
 };
-
-// MODE 2 decoder state between tiles of a segment (shared memory, owned by warp 0)
-struct DecState {
-  uint32_t x[32];     // lane states
-  uint64_t wbyte;     // byte offset of word 0 of the segment in the bitstream buffer
-  uint32_t W, used;   // words in the segment, words consumed so far
-  uint32_t bad;
-  uint32_t wbuf[66];  // the next tile's words [2 (used / 2), 2 (used / 2) + 132), prefetched by cp.async
-};
-
-__device__ __forceinline__ uint32_t ld_u32b(const uint8_t* p) {
-  return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
-}
-
-// work item: rows [base, base + rows) of the level (MODE 0/1: flat 128-row tiles;
-// MODE 2: tile t of segment seg, whole rANS steps)
-struct Wk {
-  uint32_t base, rows, t;
-  int seg, K;      // MODE 2: segment, its rANS lanes
-  bool ok, last;   // MODE 2: last tile of the segment
-};
-
-// MODE 2, warp 0: the rANS decode steps of one staged tile (the same stream contract as
-// rans.cu's k_rans_dec: lane k owns symbols s*K + k, one refill word per symbol at most,
-// words consumed in stream order; reading Q24).  At t == 0 the segment header is parsed
-// and validated; at the segment's last tile every word must be consumed and every lane
-// back at 2^16, else EF_CORRUPT.
-__device__ __noinline__ void decode_tile(const Wk cur, DecState* ds, const uint16_t* __restrict__ stage,
-                                         const int32_t* __restrict__ rowi, const DecSeg* __restrict__ segs,
-                                         const uint8_t* __restrict__ bs, uint8_t* __restrict__ Xdec,
-                                         uint32_t* __restrict__ err, int stg) {
-  const int lane = threadIdx.x & 31;
-  const int K = cur.K;
-  uint32_t x, W, used;
-  bool bad;
-  if (cur.t == 0) {  // segment header: walk the level payload's earlier full segments
-    const DecSeg sg = segs[cur.seg];
-    const uint8_t* lvl = bs + sg.byte;
-    uint32_t pos = 0;
-    bad = false;
-    for (uint32_t ch = 0; ch < sg.chunk && !bad; ++ch) {
-      if (pos + 4 > sg.level_bytes) { bad = true; break; }
-      const uint32_t Wc = ld_u32b(lvl + pos);
-      const uint64_t sz = 4ull + 128ull + 4ull * ((uint64_t(Wc) + 1) / 2);
-      if (pos + sz > sg.level_bytes) { bad = true; break; }
-      pos += uint32_t(sz);
-    }
-    W = 0;
-    if (!bad) {
-      if (uint64_t(pos) + 4 + 4 * K > sg.level_bytes) bad = true;
-      else {
-        W = ld_u32b(lvl + pos);
-        const uint64_t sz = 4ull + 4ull * K + 4ull * ((uint64_t(W) + 1) / 2);
-        if (W > sg.n || pos + sz > sg.level_bytes) bad = true;
-        if (sg.last && pos + sz != sg.level_bytes) bad = true;
-      }
-    }
-    x = (!bad && lane < K) ? ld_u32b(lvl + pos + 4 + 4 * lane) : (1u << 16);
-    if (x < (1u << 16)) bad = true;
-    bad = __any_sync(0xffffffffu, bad);
-    used = 0;
-    if (lane == 0) ds->wbyte = sg.byte + pos + 4 + 4 * K;
-  } else {
-    x = ds->x[lane];
-    W = ds->W;
-    used = ds->used;
-    bad = ds->bad != 0u;
-  }
-  if (!bad) {
-    __syncwarp();  // ds->wbyte written by lane 0 at t == 0
-    // this tile needs at most cur.rows <= 128 words: a 128-word window in 4 registers,
-    // from the words prefetched into smem by the previous tile (global at a segment start)
-    uint32_t w4[4];
-    if (cur.t == 0) {
-      const uint16_t* wp = reinterpret_cast<const uint16_t*>(bs + ds->wbyte);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t k = used + uint32_t(32 * i + lane);
-        w4[i] = k < W ? uint32_t(wp[k]) : 0u;
-      }
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      __syncwarp();
-      const uint16_t* wb = reinterpret_cast<const uint16_t*>(ds->wbuf);
-      const uint32_t k0 = used & ~1u;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t k = used + uint32_t(32 * i + lane);
-        w4[i] = k < W ? uint32_t(wb[k - k0]) : 0u;
-      }
-    }
-    const unsigned lt = (1u << lane) - 1u;
-    const uint32_t steps = (cur.rows + uint32_t(K) - 1u) / uint32_t(K);
-    uint32_t ut = 0;
-    for (uint32_t sl = 0; sl < steps; ++sl) {
-      const uint32_t r2 = sl * uint32_t(K) + uint32_t(lane);
-      const bool act = lane < K && r2 < cur.rows;
-      bool need = false;
-      if (act) {
-        const uint16_t* c = stage + r2 * uint32_t(stg);
-        const int4 o03 = *reinterpret_cast<const int4*>(rowi + r2 * 8);
-        const int2 li = *reinterpret_cast<const int2*>(rowi + r2 * 8 + 4);  // leftover, first argmax
-        auto val = [&](int i) -> uint32_t {
-          const int qq = i >> 6;
-          const int o = qq == 0 ? o03.x : (qq == 1 ? o03.y : (qq == 2 ? o03.z : o03.w));
-          return uint32_t(c[i]) + uint32_t(o) + (i > li.y ? uint32_t(li.x) : 0u);
-        };
-        const uint32_t slot = x & 0xffffu;
-        int lo = 0, hi = NCODE - 1;
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (lo < hi) {
-            if (val(mid) <= slot) lo = mid; else hi = mid - 1;
-          }
-        }
-        const uint32_t cm = val(lo);
-        const uint32_t nx = lo < NCODE - 1 ? val(lo + 1) : 65536u;
-        Xdec[cur.base + r2] = uint8_t(lo + 1);
-        x = (nx - cm) * (x >> 16) + slot - cm;
-        need = x < (1u << 16);
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, need);
-      const uint32_t off = ut + __popc(m & lt);  // < 128: at most one word per symbol of the tile
-      const uint32_t v0 = __shfl_sync(0xffffffffu, w4[0], off & 31);
-      const uint32_t v1 = __shfl_sync(0xffffffffu, w4[1], off & 31);
-      const uint32_t v2 = __shfl_sync(0xffffffffu, w4[2], off & 31);
-      const uint32_t v3 = __shfl_sync(0xffffffffu, w4[3], off & 31);
-      if (need) {
-        if (used + off < W) {
-          const uint32_t g = off >> 5;
-          x = (x << 16) | (g == 0 ? v0 : (g == 1 ? v1 : (g == 2 ? v2 : v3)));
-        } else {
-          bad = true;
-        }
-      }
-      ut += __popc(m);
-    }
-    used += ut;
-    bad = __any_sync(0xffffffffu, bad);
-  }
-  if (cur.last) {
-    if (used != W || (lane < K && x != (1u << 16))) bad = true;
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, EF_CORRUPT);
-  } else {
-    ds->x[lane] = x;
-    if (lane == 0) {
-      ds->W = W;
-      ds->used = used;
-      ds->bad = bad ? 1u : 0u;
-    }
-    // prefetch the next tile's words (u32-aligned, inside the segment's word area)
-    __syncwarp();
-    const uint32_t u0 = used >> 1, nw32 = (W + 1u) >> 1;
-    const uint8_t* src = bs + ds->wbyte;
-    for (uint32_t i = uint32_t(lane); i < 66u; i += 32u)
-      if (!bad && u0 + i < nw32)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(tc::smem_u32(&ds->wbuf[i])),
-                     "l"(src + 4ull * (u0 + i)));
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  }
-  __syncwarp();
-}
 
 // SAT = false when the model proves |z| can never reach the logit saturation thresholds
 // (checked at load from |b2| + 128 * sum|W2|): no min tracking, no saturation selects.
@@ -267,10 +99,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
                                                    const int8_t* __restrict__ W2, const int32_t* __restrict__ b2, RQ rql,
                                                    const uint32_t* __restrict__ lut, const uint8_t* __restrict__ X,
                                                    uint32_t* __restrict__ cf, uint16_t* __restrict__ cdf,
-                                                   int8_t* __restrict__ a_dbg, int32_t zsat_lo, int32_t zsat_hi,
-                                                   const DecSeg* __restrict__ segs, int nseg,
-                                                   const uint8_t* __restrict__ bs, uint8_t* __restrict__ Xdec,
-                                                   uint32_t* __restrict__ err) {
+                                                   int8_t* __restrict__ a_dbg, int32_t zsat_lo, int32_t zsat_hi) {
   extern __shared__ __align__(1024) uint8_t sm[];
   using S = SmemLayout;
   const int64_t lhalf = rql.r > 0 ? (int64_t(1) << (rql.r - 1)) : 0;
@@ -320,37 +149,14 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   const uint64_t bdesc = tc::sdesc(tc::smem_u32(sB));
   const uint32_t ntiles = (n + TILE - 1) / TILE;
   uint32_t phase = 0;
-  auto seg_work = [&](int sg, uint32_t t) -> Wk {
-    Wk w{0u, 0u, t, sg, 1, sg < nseg, false};
-    if (w.ok) {
-      const uint32_t sn = segs[sg].n, K = uint32_t(lanes_for(sn)), T = (uint32_t(TILE) / K) * K;
-      w.base = segs[sg].node + t * T;
-      w.rows = min(T, sn - t * T);
-      w.K = int(K);
-      w.last = (t + 1) * T >= sn;
-    }
-    return w;
-  };
-  auto first_work = [&]() -> Wk {
-    if constexpr (MODE == 2) return seg_work(int(blockIdx.x), 0u);
-    const uint32_t k = blockIdx.x;
-    return Wk{k * TILE, k < ntiles ? min(uint32_t(TILE), n - k * TILE) : 0u, k, 0, 1, k < ntiles, false};
-  };
-  auto next_work = [&](const Wk& w) -> Wk {
-    if constexpr (MODE == 2) {
-      return w.last ? seg_work(w.seg + int(gridDim.x), 0u) : seg_work(w.seg, w.t + 1);
-    }
-    const uint32_t k = w.t + gridDim.x;
-    return Wk{k * TILE, k < ntiles ? min(uint32_t(TILE), n - k * TILE) : 0u, k, 0, 1, k < ntiles, false};
-  };
 
   // The next tile's feature rows are copied (cp.async) into smem while this tile runs;
   // row r's chunks are copied by the row's own quarter threads q < RCH, so a row barrier
   // makes them visible to the row's 4 threads.
   constexpr int CB = C < 16 ? C : 16, RCH = C / CB;  // copy chunk, chunks per row
-  auto prefetch_f = [&](const Wk& w) {
-    const uint32_t rw = w.base + r;
-    if (w.ok && q < RCH && uint32_t(r) < w.rows) {
+  auto prefetch_f = [&](uint32_t tl) {
+    const uint32_t rw = tl * TILE + r;
+    if (tl < ntiles && q < RCH && rw < n) {
       if constexpr (CB == 16)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(sm + S::FST + r * C + 16 * q)),
                      "l"(F + size_t(rw) * C + 16 * q));
@@ -363,9 +169,9 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   // hidden layer of tile tl: this thread's H/4 units of row r, into the A operand; then the
   // logit bias b2 initialises the accumulator (columns 64q.. of row r): the MMA adds a W2^T
   // onto it, so the passes read z = b2 + a W2^T directly
-  auto hidden_and_bias = [&](const Wk& w) {
-    const uint32_t rw = w.base + r;
-    const bool vr = uint32_t(r) < w.rows;
+  auto hidden_and_bias = [&](uint32_t tl) {
+    const uint32_t rw = tl * TILE + r;
+    const bool vr = rw < n;
     int32_t fw[CW];
 #pragma unroll
     for (int w = 0; w < CW; ++w) fw[w] = vr ? reinterpret_cast<const int32_t*>(sm + S::FST + r * C)[w] : 0;
@@ -409,12 +215,11 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     }
     tmem_wait_st();
   };
-  Wk cur = first_work();
-  if (cur.ok) {
-    prefetch_f(cur);
+  if (blockIdx.x < ntiles) {
+    prefetch_f(blockIdx.x);
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     bar_rows();
-    hidden_and_bias(cur);
+    hidden_and_bias(blockIdx.x);
   }
   tc::fence_async_smem();
   tc::fence_before();
@@ -422,17 +227,16 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   tc::fence_after();
   long long tr0 = clock64();
   (void)tr0;
-  while (cur.ok) {
-    const Wk nxt = next_work(cur);
-    const uint32_t row = cur.base + r;
-    const bool valid = uint32_t(r) < cur.rows;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t row = tile * TILE + r;
+    const bool valid = row < n;
     // A operand and bias-initialised accumulator of this tile are complete (end of the
     // previous iteration / prologue)
     if (tid == 0) {
       tc::mma_i8(tbase, adesc, bdesc, IDESC, 1u);
       tc::commit(mbar);
     }
-    prefetch_f(nxt);  // the previous F rows were consumed before the barrier
+    prefetch_f(tile + gridDim.x);  // the previous F rows were consumed before the barrier
     tc::mbar_wait(mbar, phase);
     phase ^= 1u;
     tc::fence_after();
@@ -594,7 +398,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         if (istar == sym) f += left;
         cf[row] = cm | (f << 16);
       }
-    } else {  // MODE 1, 2: quarter-local cumulative rows staged in smem
+    } else {
       uint16_t* srow = stage + r * STG;
       uint32_t run = 0;
 #pragma unroll 1
@@ -631,24 +435,19 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         rowi[r * 8 + 5] = istar;
       }
       bar_rows();
-      if constexpr (MODE == 2) {
-        __syncthreads();  // every row's staging + fix-up data is visible to warp 0
-        if (warp == 0)
-          decode_tile(cur, reinterpret_cast<DecState*>(sm + S::DEC), stage, rowi, segs, bs, Xdec, err, STG);
-      } else {
       // coalesced write-out: 16 rows per iteration, 32 threads x 16 bytes per 512-byte row.
       // Packed u16 pairs: every cdf value below index 255 is < 2^16, so the quarter offset
       // and the leftover are added to both halves at once without carries; the leftover
       // goes to the elements after the first argmax: t = how many of the chunk's 8
       // elements are <= istar selects the half-word mask of each word.
-      const uint32_t rows_here = cur.rows;
+      const uint32_t rows_here = (n - tile * TILE) < uint32_t(TILE) ? (n - tile * TILE) : uint32_t(TILE);
       // rows of this warp's lane quarter only (32 * (w % 4) + w / 4 + 4 i): staged by the
       // same 128 threads, so the row barrier suffices
       const uint32_t j = uint32_t(tid) & 31u, sub = 32u * uint32_t(warp & 3) + uint32_t(warp >> 2), jq = j >> 3;
       const uint4* mask4 = reinterpret_cast<const uint4*>(sm + S::MASK);
       const uint16_t* sp = stage + sub * STG + 8 * j;
       const int32_t* rp = rowi + sub * 8;
-      uint4* gp = reinterpret_cast<uint4*>(cdf + (size_t(cur.base) + sub) * 256) + j;
+      uint4* gp = reinterpret_cast<uint4*>(cdf + (size_t(tile) * TILE + sub) * 256) + j;
       const uint32_t rend = min(rows_here, 32u * uint32_t(warp & 3) + 32u);
       for (uint32_t rr = sub; rr < rend; rr += 4, sp += 4 * STG, rp += 4 * 8, gp += 4 * 32) {
         const uint32_t offw = uint32_t(rp[jq]) * 0x10001u;
@@ -664,23 +463,20 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         if (j == 31u) o.w = (o.w & 0xffffu) | 0xffff0000u;  // index 255: padding
         *gp = o;
       }
-      }
     }
     HEAD_TRACE(5, tr0);
     // next tile: its F rows landed (own copies + row barrier), hidden layer into A and the
-    // bias into this thread's TMEM columns (all of this tile's TMEM reads are done).  In
-    // MODE 2 warp 0's most recent group is the next tile's rANS words (may stay in flight).
-    if (MODE == 2 && warp == 0 && !cur.last) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    // bias into this thread's TMEM columns (all of this tile's TMEM reads are done)
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     bar_rows();
-    if (nxt.ok) hidden_and_bias(nxt);
+    if (tile + gridDim.x < ntiles) hidden_and_bias(tile + gridDim.x);
     HEAD_TRACE(0, tr0);
     tc::fence_async_smem();
     tc::fence_before();
     __syncthreads();  // A operand + bias complete; stage / red / rowi reused by the next tile
+    tc::fence_after();
     HEAD_TRACE(6, tr0);
     tc::fence_after();
-    cur = nxt;
   }
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<256>(tbase);
@@ -729,18 +525,17 @@ __global__ void __launch_bounds__(128) k_gemm_i8_test(const int8_t* __restrict__
 
 template <int C, int H, int MODE, bool SAT>
 void launch_head(pcc_ctx c, const int8_t* F, uint32_t n, const DHead& L, const uint32_t* lut, const uint8_t* X,
-                 uint32_t* cf, uint16_t* cdf, int8_t* a_dbg, const DecSeg* segs = nullptr, int nseg = 0,
-                 const uint8_t* bs = nullptr, uint8_t* Xdec = nullptr, uint32_t* err = nullptr) {
+                 uint32_t* cf, uint16_t* cdf, int8_t* a_dbg) {
   auto kern = k_head_tc<C, H, MODE, SAT>;
   static bool attr = false;
   if (!attr) {
     PCC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemLayout::END));
     attr = true;
   }
-  const uint32_t units = MODE == 2 ? uint32_t(nseg) : (n + TILE - 1) / TILE;  // segments or tiles
-  const unsigned grid = std::max(1u, std::min(units, unsigned(c->sm_count) * 2u));
+  const uint32_t ntiles = (n + TILE - 1) / TILE;
+  const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 2u));
   kern<<<grid, NT, SmemLayout::END, c->stream>>>(F, n, L.W1, L.b1, L.rq1, L.W2, L.b2, L.rql, lut, X, cf, cdf, a_dbg,
-                                                 L.zsat_lo, L.zsat_hi, segs, nseg, bs, Xdec, err);
+                                                 L.zsat_lo, L.zsat_hi);
   launched(c);
 }
 
@@ -765,25 +560,6 @@ void head_cdf_tc(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHe
   throw Error{PCC_ERR_INVALID_ARG};
 }
 
-void head_decode_fused(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut,
-                       const DecSeg* d_segs, int nseg, const uint8_t* bs, uint8_t* X, uint32_t* err) {
-  if (n == 0 || nseg == 0) return;
-  Prof p(c, "head_dec", size_t(n) * (C + 1));
-#define PCC_HEAD(CC)                                                                                      \
-  if (C == CC && H == CC) {                                                                               \
-    if (L.can_saturate)                                                                                   \
-      launch_head<CC, CC, 2, true>(c, F, n, L, lut, nullptr, nullptr, nullptr, nullptr, d_segs, nseg, bs, X, err); \
-    else                                                                                                  \
-      launch_head<CC, CC, 2, false>(c, F, n, L, lut, nullptr, nullptr, nullptr, nullptr, d_segs, nseg, bs, X, err); \
-    return;                                                                                               \
-  }
-  PCC_HEAD(8)
-  PCC_HEAD(16)
-  PCC_HEAD(32)
-#undef PCC_HEAD
-  throw Error{PCC_ERR_INVALID_ARG};
-}
-
 void gemm_i8_test(pcc_ctx c, const int8_t* dA, const int8_t* dB, int N, int32_t* dD) {
   if (N < 32 || N > 256 || N % 32) throw Error{PCC_ERR_INVALID_ARG};
   static bool attr = false;
@@ -799,9 +575,9 @@ void gemm_i8_test(pcc_ctx c, const int8_t* dA, const int8_t* dB, int N, int32_t*
 
 #ifdef PCC_TRACE
 extern "C" int pcc_trace_head(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, pcc::g_head_trace, sizeof(unsigned long long) * 24);
+  cudaMemcpyFromSymbol(out, pcc::g_head_trace, sizeof(unsigned long long) * 16);
   if (reset) {
-    unsigned long long z[24] = {};
+    unsigned long long z[16] = {};
     cudaMemcpyToSymbol(pcc::g_head_trace, z, sizeof(z));
   }
   return 0;

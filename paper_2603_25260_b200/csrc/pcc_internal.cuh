@@ -15,11 +15,6 @@ namespace pcc {
 constexpr int NCODE = 255;     // occupancy classes
 constexpr int SEG_SYMS = 16384; // rANS segment length (reading Q24: <= 512 steps per lane)
 constexpr int MAX_LANES = 32;
-// lanes of a segment of n symbols (reading Q24): K = clamp(ceil(n / 512), 1, 32)
-__host__ __device__ inline int lanes_for(uint32_t n) {
-  const uint32_t k = (n + 511u) / 512u;
-  return int(k < 1u ? 1u : (k > 32u ? 32u : k));
-}
 constexpr int MAX_DEPTH = 21;   // 63-bit Morton key cap
 
 // Device error flags (atomicOr'ed by kernels, read at sync points).
@@ -236,10 +231,6 @@ struct DecSeg {
 };
 void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf, uint8_t* X,
                  uint32_t* err, int max_lanes);
-// fused decoder (head_tc.cu MODE 2): predictor + integer softmax + rANS decode per
-// segment, the cumulative rows kept in shared memory
-void head_decode_fused(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut,
-                       const DecSeg* d_segs, int nseg, const uint8_t* bs, uint8_t* X, uint32_t* err);
 
 // ---- pack (runtime.cu) ----
 struct PackItem {    // encoder output item: frame header+raw prefix (kind 0) or one segment (kind 1)

@@ -10,6 +10,11 @@ namespace pcc {
 
 namespace {
 
+__device__ __forceinline__ int lanes_for(uint32_t n) {
+  uint32_t k = (n + 511u) / 512u;
+  return int(k < 1u ? 1u : (k > 32u ? 32u : k));
+}
+
 __global__ void __launch_bounds__(128) k_rans_enc(const EncSeg* __restrict__ segs, int nseg, const uint32_t* __restrict__ cf,
                                                   uint16_t* __restrict__ words, uint32_t* __restrict__ seg_W,
                                                   uint32_t* __restrict__ seg_state) {

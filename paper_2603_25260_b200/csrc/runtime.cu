@@ -113,20 +113,9 @@ void head_any(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead&
   else head_cdf_tc(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
 }
 
-
-// Decoder per level: the fused predictor+rANS kernel (head_tc.cu MODE 2) when the level
-// has enough segments to occupy the GPU, else the two-kernel path (predictor writes CDF
-// rows, k_rans_dec reads them).  PCC_DEC_FUSED=0/1 forces either (A/B and tests);
-// PCC_HEAD=simt implies the two-kernel path.
-bool use_fused_decoder(size_t nseg) {
-  static const int mode = [] {
-    const char* h = getenv("PCC_HEAD");
-    if (h && std::string(h) == "simt") return 0;
-    const char* e = getenv("PCC_DEC_FUSED");
-    return e ? atoi(e) : -1;
-  }();
-  if (mode >= 0) return mode != 0;
-  return nseg >= 32;
+inline int lanes_for(uint32_t n) {
+  uint32_t k = (n + 511u) / 512u;
+  return int(k < 1u ? 1u : (k > 32u ? 32u : k));
 }
 
 // ============================================================================
@@ -885,6 +874,13 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
   for (int d = R; d < L; ++d) {
     const int8_t* Fd = net.level(d);
     const uint32_t nd = o.N[d];
+    uint16_t* cdf = buf<uint16_t>(c, "cdf", size_t(nd) * 256);
+    int8_t* a_dbg = c->debug ? buf<int8_t>(c, "t_adbg", size_t(nd) * m->H) : nullptr;
+    head_any(c, Fd, nd, C, m->H, net.head_of(d), m->lut, 1, nullptr, nullptr, cdf, a_dbg);
+    if (c->debug) {
+      dbg_copy(c, nm("a", d), a_dbg, size_t(nd) * m->H);
+      dbg_copy(c, nm("cdf", d), cdf, size_t(nd) * 512);
+    }
     std::vector<DecSeg> segs;
     for (int f = 0; f < B; ++f) {
       const uint32_t a = o.foff[size_t(d) * (B + 1) + f], nfd = o.foff[size_t(d) * (B + 1) + f + 1] - a;
@@ -895,26 +891,11 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
       }
       lvl_base[f] += hd[f].lb[d - R];
     }
-    uint8_t* Xd = static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d];
-    if (!c->debug && use_fused_decoder(segs.size())) {
-      // predictor + softmax + rANS in one kernel per level, the CDF rows kept on chip;
-      // longest segments first so the persistent CTAs finish together
-      std::stable_sort(segs.begin(), segs.end(), [](const DecSeg& a, const DecSeg& b) { return a.n > b.n; });
-      DecSeg* d_segs = upload(c, "dsegs", segs);
-      head_decode_fused(c, Fd, nd, C, m->H, net.head_of(d), m->lut, d_segs, int(segs.size()), d_bs, Xd, err);
-    } else {
-      uint16_t* cdf = buf<uint16_t>(c, "cdf", size_t(nd) * 256);
-      int8_t* a_dbg = c->debug ? buf<int8_t>(c, "t_adbg", size_t(nd) * m->H) : nullptr;
-      head_any(c, Fd, nd, C, m->H, net.head_of(d), m->lut, 1, nullptr, nullptr, cdf, a_dbg);
-      if (c->debug) {
-        dbg_copy(c, nm("a", d), a_dbg, size_t(nd) * m->H);
-        dbg_copy(c, nm("cdf", d), cdf, size_t(nd) * 512);
-      }
-      DecSeg* d_segs = upload(c, "dsegs", segs);
-      int kmax = 1;
-      for (const DecSeg& sg : segs) kmax = std::max(kmax, lanes_for(sg.n));
-      rans_decode(c, d_segs, int(segs.size()), d_bs, cdf, Xd, err, kmax);
-    }
+    DecSeg* d_segs = upload(c, "dsegs", segs);
+    int kmax = 1;
+    for (const DecSeg& sg : segs) kmax = std::max(kmax, lanes_for(sg.n));
+    rans_decode(c, d_segs, int(segs.size()), d_bs, cdf, static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d], err,
+                kmax);
     PCC_CUDA(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s));
     PCC_CUDA(cudaStreamSynchronize(s));
     if (herr) throw Error{PCC_ERR_CORRUPT};

@@ -392,74 +392,3 @@ def test_alternate_kernels_bit_exact(pcc, env):
     r = subprocess.run([sys.executable, "-c", _ALT.format(root=root)], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert "ALT-OK" in r.stdout, r.stdout + r.stderr
-
-
-# ---------------------------------------------------------------------------------------
-# fused decoder (predictor + softmax + rANS in one kernel per level, head_tc.cu MODE 2)
-# against the oracle, forced on for every level; and the two-kernel path forced on
-# ---------------------------------------------------------------------------------------
-
-_FUSED = r"""
-import sys, numpy as np, torch
-sys.path.insert(0, {root!r})
-from oracle import oracle as O
-from paper_2603_25260_b200 import inputs as I, pcc
-cases = [
-    (8, [I.make_frame(I.CFG1), I.random_cloud(3000, 10, 5, spread=0.3), I.random_cloud(40, 10, 6)], 12),
-    (32, I.make_frames(I.CFG2, 2, first=3, scene_seed=1), 12),
-    (16, [I.random_cloud(60000, 12, 9)], 12),   # levels of 2-4 rANS segments (chunk > 0)
-    (32, [I.random_cloud(20000, 18, 11, spread=0.2)], 18),
-]
-for C, frames, L in cases:
-    mb = I.make_model(C=C, H=C, seed=1, min_depth=9, max_depth=18).to_bytes()
-    om = O.Model(mb)
-    codec = pcc.Codec(mb, 0)
-    offs = np.cumsum([0] + [len(f) for f in frames]).tolist()
-    x = torch.from_numpy(np.concatenate(frames)).cuda()
-    out, oo = codec.encode_frames(x, offs, L)
-    xyz, no = codec.decode_frames(out, oo, offs[-1])
-    host = out[:oo[-1]].cpu().numpy().tobytes()
-    for i in range(len(frames)):
-        bs = host[oo[i]:oo[i + 1]]
-        assert bs == O.encode(om, frames[i], L), (C, L, i)
-        want = O.decode(om, bs)[0]
-        got = xyz[no[i]:no[i + 1]].cpu().numpy()
-        assert np.array_equal(got, want), (C, L, i)
-# corrupt streams: the same verdict as the oracle, never a hang
-mb = I.make_model(C=8, H=8, seed=1, min_depth=9, max_depth=12).to_bytes()
-om = O.Model(mb)
-codec = pcc.Codec(mb, 0)
-pts = I.random_cloud(800, 10, 2)
-bs = O.encode(om, pts, 10)
-rng = np.random.default_rng(11)
-for _ in range(60):
-    d = bytearray(bs)
-    pos = int(rng.integers(24, len(d)))
-    d[pos] ^= 1 << int(rng.integers(0, 8))
-    d = bytes(d) + bytes((-len(d)) % 4)
-    try:
-        want = O.decode(om, d[:len(bs)])[0]
-    except O.OracleError as e:
-        want = e.name
-    try:
-        xyz, no = codec.decode_frames(torch.from_numpy(np.frombuffer(d, np.uint8).copy()).cuda(), [0, len(d)], 4096)
-        got = xyz[:no[1]].cpu().numpy()
-    except pcc.PCCError as e:
-        got = e.name
-    if isinstance(want, str):
-        assert got in ("CORRUPT", "TRUNCATED"), (want, got)
-    else:
-        assert not isinstance(got, str) and np.array_equal(got, want)
-print("FUSED-OK")
-"""
-
-
-@pytest.mark.parametrize("fused", ["1", "0"])
-def test_fused_decoder_bit_exact(pcc, fused):
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", _FUSED.format(root=root)], env={**os.environ, "PCC_DEC_FUSED": fused},
-                       capture_output=True, text=True, timeout=900)
-    assert "FUSED-OK" in r.stdout, r.stdout + r.stderr

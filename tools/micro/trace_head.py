@@ -27,16 +27,16 @@ x = torch.from_numpy(np.concatenate(frames)).cuda()
 bs, oo = codec.encode_frames(x, offs, 12)
 codec.decode_frames(bs, oo, offs[-1])
 torch.cuda.synchronize()
-buf = (ct.c_ulonglong * 24)()
+buf = (ct.c_ulonglong * 16)()
 lib.pcc_trace_head(buf, 1)
 bs, oo = codec.encode_frames(x, offs, 12)
 codec.decode_frames(bs, oo, offs[-1])
 torch.cuda.synchronize()
 lib.pcc_trace_head(buf, 0)
 names = ["hidden+bias+bar", "mma wait", "pass1+bar", "pass2+bars", "pass3 (+stage)", "tail/write-out", "end barrier"]
-for mode in (0, 1, 2):
+for mode in (0, 1):
     v = buf[8 * mode: 8 * mode + 7]
     tot = sum(v) or 1
-    print(["encoder", "decoder", "fused decoder"][mode])
+    print("encoder" if mode == 0 else "decoder")
     for i, nme in enumerate(names):
         print(f"  {nme:18s} {v[i] / 1e6:10.2f} Mcyc  {100 * v[i] / tot:5.1f}%")
