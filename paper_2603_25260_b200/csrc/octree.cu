@@ -53,148 +53,134 @@ __global__ void k_morton(const int32_t* __restrict__ xyz, size_t n, const uint64
   keys[i] = (B > 1 ? (uint64_t(lo) << (3 * L)) : 0ull) | m;
 }
 
-// ---- radix sort (LSD, 8-bit digits, stable per pass) ---------------------------------
+// ---- radix sort (LSD, 8- or 9-bit digits, stable per pass, frame-segmented) ----------
+// The input keys are frame-contiguous (frame f = points offs[f]..offs[f+1]) and carry the
+// frame id above bit 3L, so only the 3L Morton bits are sorted: every tile lies inside
+// one frame, and the per-tile digit counts are laid out frame-major, digit-major,
+// tile-minor (hist[256 T0_f + d nt_f + (g - T0_f)] for tile g of frame f, whose tiles
+// are T0_f .. T0_f + nt_f), so one exclusive scan of the whole array gives every
+// (frame, digit, tile) its output offset and the frames stay where they were.
 constexpr int RS_T = 256, RS_V = 16, RS_TILE = RS_T * RS_V, RS_W = RS_T / 32;
 
-// ---- onesweep radix pass (decoupled look-back): one read + one write of the keys per
-// digit.  The global digit histograms of every pass come from one upfront read
-// (k_rs_ghist); each tile takes its id from an atomic counter (so every predecessor is
-// running), ranks its keys per digit (warp match_any, stable), publishes its
-// per-digit count (flag AGG), looks back over predecessors until an inclusive prefix
-// (flag INC) and publishes its own inclusive prefix, then scatters through smem.
-constexpr uint32_t OS_AGG = 1u << 30, OS_INC = 2u << 30, OS_CNT = (1u << 30) - 1u;
-constexpr int GH_MAXP = 8;  // passes covered by the global histogram (64-bit keys)
-
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+struct __align__(16) RsTile {  // tile g -> its frame's key range and histogram geometry
+  uint32_t start, count, T0, nt;
+};
+// once per sort: one thread per tile
+__global__ void k_rs_tiles(const uint32_t* __restrict__ tp, const uint64_t* __restrict__ offs, int B, uint32_t ntiles,
+                           RsTile* __restrict__ tiles) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ntiles) return;
+  int lo = 0, hi = B - 1;  // frame: largest f < B with tp[f] <= g
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tp[mid] <= g) lo = mid; else hi = mid - 1;
+  }
+  RsTile t;
+  t.T0 = tp[lo];
+  t.nt = tp[lo + 1] - t.T0;
+  t.start = uint32_t(offs[lo]) + (g - t.T0) * uint32_t(RS_TILE);
+  t.count = min(uint32_t(RS_TILE), uint32_t(offs[lo + 1]) - t.start);
+  tiles[g] = t;
 }
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
-// hist[p][d] += #keys with digit p == d, for p < npass (grid-stride, block-private smem
-// histograms, one global atomic per (block, pass, digit))
-__global__ void __launch_bounds__(256) k_rs_ghist(const uint64_t* __restrict__ keys, size_t n, int npass,
-                                                  uint32_t* __restrict__ hist) {
-  __shared__ uint32_t h[GH_MAXP][256];
-  for (int i = threadIdx.x; i < GH_MAXP * 256; i += 256) (&h[0][0])[i] = 0;
+template <int DB>
+__global__ void __launch_bounds__(RS_T) k_rs_hist(const uint64_t* __restrict__ keys, int shift,
+                                                  const RsTile* __restrict__ tiles, uint32_t* __restrict__ hist) {
+  constexpr int ND = 1 << DB;
+  constexpr uint32_t MASK = ND - 1;
+  __shared__ uint32_t h[ND];
+  for (int i = threadIdx.x; i < ND; i += RS_T) h[i] = 0;
+  const RsTile t = tiles[blockIdx.x];
   __syncthreads();
-  for (size_t i = size_t(blockIdx.x) * 256 + threadIdx.x; i < n; i += size_t(gridDim.x) * 256) {
-    const uint64_t k = keys[i];
-    for (int p = 0; p < npass; ++p) atomicAdd(&h[p][uint32_t(k >> (8 * p)) & 255u], 1u);
+#pragma unroll 4
+  for (int k = 0; k < RS_V; ++k) {
+    const uint32_t i = uint32_t(k) * RS_T + threadIdx.x;
+    const uint32_t d = i < t.count ? uint32_t(keys[t.start + i] >> shift) & MASK : uint32_t(ND);
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (d < uint32_t(ND) && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[d], __popc(peers));
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < npass * 256; i += 256) {
-    const uint32_t v = (&h[0][0])[i];
-    if (v) atomicAdd(&hist[i], v);
-  }
+  const size_t hb = size_t(ND) * t.T0 + (blockIdx.x - t.T0);
+  for (int d = threadIdx.x; d < ND; d += RS_T) hist[hb + size_t(d) * t.nt] = h[d];
 }
 
-// hist[p][256] -> exclusive prefix over digits, in place (one warp per pass)
-__global__ void k_rs_gbase(uint32_t* __restrict__ hist, int npass) {
-  const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (p >= npass) return;
-  uint32_t* h = hist + p * 256;
-  uint32_t v[8], s = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) s += (v[k] = h[lane * 8 + k]);
-  uint32_t inc = s;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += t;
-  }
-  uint32_t run = inc - s;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    h[lane * 8 + k] = run;
-    run += v[k];
-  }
-}
-
-__global__ void __launch_bounds__(RS_T) k_rs_onesweep(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
-                                                      size_t n, int shift, const uint32_t* __restrict__ gbase,
-                                                      uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr) {
-  __shared__ uint32_t wc[RS_W][257];
-  __shared__ uint32_t tstart[256];
-  __shared__ uint32_t gofs[256];
+template <int DB>
+__global__ void __launch_bounds__(RS_T) k_rs_scatter(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                                     int shift, const RsTile* __restrict__ tiles,
+                                                     const uint32_t* __restrict__ hscan) {
+  constexpr int ND = 1 << DB, DPT = ND / RS_T;  // digits per thread in the per-digit phases
+  constexpr uint32_t MASK = ND - 1;
+  __shared__ uint16_t wc[RS_W][ND + 1];  // per-warp digit counts, then offsets (< RS_TILE)
+  __shared__ uint32_t tstart[ND];
+  __shared__ uint32_t gbase[ND];
   __shared__ uint32_t wtot[RS_W];
-  __shared__ uint32_t s_tile;
   __shared__ uint64_t stage[RS_TILE];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  for (int i = threadIdx.x; i < RS_W * 257; i += RS_T) (&wc[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < RS_W * (ND + 1); i += RS_T) (&wc[0][0])[i] = 0;
+  const RsTile t = tiles[blockIdx.x];
   __syncthreads();
-  const uint32_t tile = s_tile;
   const unsigned lt = (1u << lane) - 1u;
   uint64_t kv[RS_V];
   uint32_t rk[RS_V];
-  const size_t wbase = size_t(tile) * RS_TILE + size_t(w) * (RS_TILE / RS_W);
+  const uint32_t wbase = uint32_t(w) * (RS_TILE / RS_W);
 #pragma unroll
-  for (int t = 0; t < RS_V; ++t) {
-    const size_t i = wbase + size_t(t) * 32 + lane;
-    const uint64_t k = i < n ? in[i] : 0ull;
-    const uint32_t d = i < n ? uint32_t((k >> shift) & 255u) : 256u;
+  for (int v = 0; v < RS_V; ++v) {
+    const uint32_t i = wbase + uint32_t(v) * 32 + lane;
+    const uint64_t k = i < t.count ? in[t.start + i] : 0ull;
+    const uint32_t d = i < t.count ? uint32_t(k >> shift) & MASK : uint32_t(ND);
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const uint32_t base = wc[w][d];
     __syncwarp();
-    if (lane == __ffs(peers) - 1) wc[w][d] = base + __popc(peers);
+    if (lane == __ffs(peers) - 1) wc[w][d] = uint16_t(base + __popc(peers));
     __syncwarp();
-    kv[t] = k;
-    rk[t] = (d << 16) | (base + __popc(peers & lt));
+    kv[v] = k;
+    rk[v] = (d << 16) | (base + __popc(peers & lt));  // rank < 4096 fits 16 bits
   }
   __syncthreads();
-  const uint32_t d = threadIdx.x;  // one thread per digit from here
-  uint32_t run = 0;
-  for (int ww = 0; ww < RS_W; ++ww) {
-    const uint32_t t = wc[ww][d];
-    wc[ww][d] = run;
-    run += t;
-  }
-  // publish this tile's count, look back for the exclusive prefix over earlier tiles
-  uint32_t* st = status + size_t(tile) * 256 + d;
-  uint32_t excl = 0;
-  if (tile == 0) {
-    st_release(st, OS_INC | run);
-  } else {
-    st_release(st, OS_AGG | run);
-    for (int64_t t = int64_t(tile) - 1; t >= 0;) {
-      const uint32_t v = ld_acquire(status + size_t(t) * 256 + d);
-      if ((v & ~OS_CNT) == 0u) continue;  // predecessor not published yet
-      excl += v & OS_CNT;
-      if (v & OS_INC) break;
-      --t;
+  // per digit: exclusive prefix over warps and the tile count; this thread owns digits
+  // DPT * tid .. DPT * tid + DPT - 1 (consecutive, so the block scan is in digit order)
+  uint32_t cnt[DPT], s = 0;
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int d = DPT * threadIdx.x + j;
+    uint32_t run = 0;
+    for (int ww = 0; ww < RS_W; ++ww) {
+      const uint32_t c = wc[ww][d];
+      wc[ww][d] = uint16_t(run);
+      run += c;
     }
-    st_release(st, OS_INC | (excl + run));
+    cnt[j] = run;
+    s += run;
   }
-  // exclusive scan of the tile's digit counts -> start of each digit in the staged tile
-  uint32_t inc = run;
+  uint32_t inc = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += t;
+    const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += x;
   }
   if (lane == 31) wtot[w] = inc;
   __syncthreads();
-  uint32_t wpre = 0;
-  for (int ww = 0; ww < w; ++ww) wpre += wtot[ww];
-  tstart[d] = wpre + inc - run;
-  gofs[d] = gbase[d] + excl;
-  __syncthreads();
+  uint32_t pre = inc - s;
+  for (int ww = 0; ww < w; ++ww) pre += wtot[ww];
+  const size_t hb = size_t(ND) * t.T0 + (blockIdx.x - t.T0);
 #pragma unroll
-  for (int t = 0; t < RS_V; ++t) {
-    const uint32_t dd = rk[t] >> 16;
-    if (dd < 256u) stage[tstart[dd] + wc[w][dd] + (rk[t] & 0xffffu)] = kv[t];
+  for (int j = 0; j < DPT; ++j) {
+    const int d = DPT * threadIdx.x + j;
+    tstart[d] = pre;
+    pre += cnt[j];
+    gbase[d] = hscan[hb + size_t(d) * t.nt];
   }
   __syncthreads();
-  const size_t tb = size_t(tile) * RS_TILE;
-  const uint32_t nvalid = uint32_t((n - tb) < size_t(RS_TILE) ? (n - tb) : size_t(RS_TILE));
-  for (uint32_t q = threadIdx.x; q < nvalid; q += RS_T) {
-    const uint64_t k = stage[q];
-    const uint32_t dd = uint32_t((k >> shift) & 255u);
-    out[gofs[dd] + q - tstart[dd]] = k;
+#pragma unroll
+  for (int v = 0; v < RS_V; ++v) {
+    const uint32_t d = rk[v] >> 16;
+    if (d < uint32_t(ND)) stage[tstart[d] + wc[w][d] + (rk[v] & 0xffffu)] = kv[v];
+  }
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < t.count; p += RS_T) {
+    const uint64_t k = stage[p];
+    const uint32_t d = uint32_t(k >> shift) & MASK;
+    out[gbase[d] + p - tstart[d]] = k;
   }
 }
 
@@ -374,7 +360,8 @@ void build_octree(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int B, in
   cudaStream_t s = c->stream;
   // device copy of frame offsets
   uint64_t* d_offs = wsT<uint64_t>(c, "oct_offs", B + 1);
-  uint64_t* h = static_cast<uint64_t*>(pinned(c, (B + 1) * sizeof(uint64_t)));
+  // pinned staging: offs (u64) then the sort's per-frame first tiles (u32)
+  uint64_t* h = static_cast<uint64_t*>(pinned(c, (B + 1) * (sizeof(uint64_t) + sizeof(uint32_t))));
   for (int f = 0; f <= B; ++f) h[f] = offs[f];
   PCC_CUDA(cudaMemcpyAsync(d_offs, h, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   uint32_t* err = wsT<uint32_t>(c, "err", 4);
@@ -388,28 +375,41 @@ void build_octree(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int B, in
     launched(c);
   }
 
-  int fb = 0;
-  while ((1 << fb) < B) ++fb;
-  const int bits = 3 * L + fb;
-  const uint32_t ntiles = cdiv(n, RS_TILE);
-  const int npass = (bits + 7) / 8;
-  // global digit histograms (one read), then one onesweep pass per digit
-  uint32_t* gh = wsT<uint32_t>(c, "rs_ghist", size_t(GH_MAXP) * 256 + GH_MAXP);
-  uint32_t* status = wsT<uint32_t>(c, "rs_status", size_t(npass) * ntiles * 256);
-  uint32_t* ctr = gh + size_t(GH_MAXP) * 256;
-  PCC_CUDA(cudaMemsetAsync(gh, 0, (size_t(GH_MAXP) * 256 + GH_MAXP) * sizeof(uint32_t), s));
-  PCC_CUDA(cudaMemsetAsync(status, 0, size_t(npass) * ntiles * 256 * sizeof(uint32_t), s));
+  // frame-aligned tiles: tp[f] = first tile of frame f (host copy of offs -> device)
+  uint32_t* htp = reinterpret_cast<uint32_t*>(h + (B + 1));
+  htp[0] = 0;
+  for (int f = 0; f < B; ++f) htp[f + 1] = htp[f] + cdiv(offs[f + 1] - offs[f], RS_TILE);
+  const uint32_t ntiles = htp[B];
+  uint32_t* d_tp = wsT<uint32_t>(c, "rs_tp", B + 1);
+  PCC_CUDA(cudaMemcpyAsync(d_tp, htp, (B + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  RsTile* tiles = wsT<RsTile>(c, "rs_tiles", ntiles);
   {
-    Prof p(c, "sort", n * 8);
-    k_rs_ghist<<<std::min<unsigned>(ntiles, unsigned(c->sm_count) * 4u), 256, 0, s>>>(ka, n, npass, gh);
-    k_rs_gbase<<<1, 32 * GH_MAXP, 0, s>>>(gh, npass);
-    launched(c, 2);
-  }
-  for (int ps = 0; ps < npass; ++ps) {
-    Prof p(c, "sort", n * 16);
-    k_rs_onesweep<<<ntiles, RS_T, 0, s>>>(ka, kb, n, 8 * ps, gh + ps * 256, status + size_t(ps) * ntiles * 256,
-                                          ctr + ps);
+    Prof p(c, "sort", 0);
+    k_rs_tiles<<<cdiv(ntiles, 256), 256, 0, s>>>(d_tp, d_offs, B, ntiles, tiles);
     launched(c);
+  }
+  // 3L Morton bits in 8- or 9-bit digits, whichever needs fewer passes
+  const int bits = 3 * L;
+  static const int db_forced = [] {
+    const char* e = getenv("PCC_SORT_DB");  // development override (8 or 9)
+    return e ? atoi(e) : 0;
+  }();
+  const int DB = db_forced == 8 || db_forced == 9 ? db_forced : ((bits + 8) / 9 < (bits + 7) / 8 ? 9 : 8);
+  uint32_t* hist = wsT<uint32_t>(c, "rs_hist", (size_t(1) << DB) * ntiles + 1);
+  for (int sh = 0; sh < bits; sh += DB) {
+    {
+      Prof p(c, "sort", n * 8);
+      if (DB == 9) k_rs_hist<9><<<ntiles, RS_T, 0, s>>>(ka, sh, tiles, hist);
+      else k_rs_hist<8><<<ntiles, RS_T, 0, s>>>(ka, sh, tiles, hist);
+      launched(c);
+    }
+    scan_u32(c, hist, hist, (size_t(1) << DB) * ntiles);
+    {
+      Prof p(c, "sort", n * 16);
+      if (DB == 9) k_rs_scatter<9><<<ntiles, RS_T, 0, s>>>(ka, kb, sh, tiles, hist);
+      else k_rs_scatter<8><<<ntiles, RS_T, 0, s>>>(ka, kb, sh, tiles, hist);
+      launched(c);
+    }
     std::swap(ka, kb);
   }
   const uint64_t* sorted = ka;
