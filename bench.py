@@ -9,6 +9,11 @@ SURVEY.md §8(a).  Frames shard by index across ranks (weak scaling, no data-pat
 collective); NCCL only gathers per-rank stats.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+                    [--workload cfg2|cfg3|cfg1]
+
+--workload selects another BASELINE.json config (the default, cfg2, is the one `metric`
+is quoted on): cfg3 = Ford-shaped 18-bit frames (~87k voxels, deep sparse levels), cfg1 =
+16-beam 12-bit frames with the 8-channel model.
 """
 from __future__ import annotations
 
@@ -27,7 +32,19 @@ import numpy as np  # noqa: E402
 
 METRIC = "enc/dec frames/s at 1/2/4/8 B200; bit-exact bitstream vs CPU oracle; bpp"
 UNIT = "frames/s"
-WORKLOAD = "cfg2: KITTI-shaped 64x2048 LiDAR frames (synthetic ray-cast), L=12, C=H=32 GRED+XFP int8 model"
+WORKLOADS = {  # name -> (channels C = H, description)
+    "cfg2": (32, "cfg2: KITTI-shaped 64x2048 LiDAR frames (synthetic ray-cast), L=12, C=H=32 GRED+XFP int8 model"),
+    "cfg3": (32, "cfg3: Ford-shaped 64-beam 18-bit LiDAR frames (synthetic ray-cast), L=18, C=H=32 GRED+XFP int8 model"),
+    "cfg1": (8, "cfg1: 16-beam x 512 LiDAR frames (synthetic ray-cast), L=12, C=H=8 int8 model"),
+}
+WORKLOAD = WORKLOADS["cfg2"][1]
+
+
+def workload(args):
+    """(ScanConfig, C, description) of --workload."""
+    from paper_2603_25260_b200 import inputs as I
+    C, desc = WORKLOADS[args.workload]
+    return I.CONFIGS[args.workload], C, desc
 
 
 def peaks():
@@ -124,9 +141,10 @@ def oracle_rate(frames, L, model_bytes, threads: int):
     return len(frames) / dt, dt
 
 
-def run_config(B, world):
+def run_config(args, world):
     """The workload both arms report (identical dicts: the driver compares like with like)."""
-    return {"workload": WORKLOAD, "frames_per_gpu_per_step": B, "global_batch": B * world,
+    B = args.batch
+    return {"workload": WORKLOADS[args.workload][1], "frames_per_gpu_per_step": B, "global_batch": B * world,
             "parallelism": f"frames/dp{world}", "l2": "flushed between steps (256 MiB write, outside the events)"}
 
 
@@ -134,8 +152,8 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from paper_2603_25260_b200 import inputs as I
-    cfg = I.CFG2
-    mb = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18).to_bytes()
+    cfg, C, _ = workload(args)
+    mb = I.make_model(C=C, H=C, seed=1, min_depth=9, max_depth=18).to_bytes()
     cores = max(1, min(os.cpu_count() or 1, 8))
     frames, _ = make_inputs(cfg, cores, 0)
     for _ in range(args.warmup):
@@ -149,9 +167,9 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64 (scalar CPU)",
-            "data": "synthetic", "config": run_config(args.batch, world),
+            "data": "synthetic", "config": run_config(args, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"each step a bounded sample of the workload: {cores} of its cfg2 frames "
+                             "sample": f"each step a bounded sample of the workload: {cores} of its {args.workload} frames "
                                        f"(encode+decode), one frame per thread"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -206,7 +224,8 @@ ALU_PEAK_NOTE = ("B200 integer issue peak = 148 SM x 4 SMSP x 32 lanes x 1 instr
 # hidden layer C*H/4 dp4a (C = H = 32) + 12 ops per symbol (logit requant mul-add, shift,
 # saturate; max; delta; LUT index/load/select; sum; scale multiply; quotient; correction;
 # accumulate) x 255; the decoder adds the prefix-sum store (13 per symbol).
-ALU_OPS_PER_NODE = {"head_enc": 32 * 32 / 4 + 12 * 255, "head_dec": 32 * 32 / 4 + 13 * 255}
+def alu_ops_per_node(C, H):
+    return {"head_enc": C * H / 4 + 12 * 255, "head_dec": C * H / 4 + 13 * 255}
 
 
 def measured_traffic(kernel: str):
@@ -227,11 +246,11 @@ def run_ours(args, rank, world, dist):
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
-    cfg = I.CFG2
+    cfg, C, _ = workload(args)
     L = cfg.bit_depth
     B = args.batch
     S = max(1, min(args.streams, B))
-    mb = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18).to_bytes()
+    mb = I.make_model(C=C, H=C, seed=1, min_depth=9, max_depth=18).to_bytes()
     frames, offs = make_inputs(cfg, B, shard_frames(rank, world, B)[0])
     npts = offs[-1]
     host_xyz = torch.from_numpy(np.concatenate(frames).astype(np.int32)).pin_memory()
@@ -399,6 +418,7 @@ def run_ours(args, rank, world, dist):
         for i in range(len(offs_l) - 1):
             cnt = pcc.pcc_build_octree(lanes[0].ctx, xyz_l[offs_l[i]:offs_l[i + 1]], offs_l[i + 1] - offs_l[i], L)
             coded_per_step += sum(cnt[4:L])
+    ops_per_node = alu_ops_per_node(C, C)
 
     # ---- gather per-rank stats (the only collective) ----
     stats = rank_stats(B, npts, nvox, nbytes, enc_ms, dec_ms, parity, e2e_ms)
@@ -417,10 +437,10 @@ def run_ours(args, rank, world, dist):
         name, v = top
         sec = v["ms_per_step"] / 1e3
         traffic, traffic_note = measured_traffic(name)
-        if name in ALU_OPS_PER_NODE:
+        if name in ops_per_node:
             # integer-ALU bound: algorithmic ops per coded node x coded nodes per step
             sm_max = float(pk.get("sm_max_mhz", 1965.0))
-            achieved = coded_per_step * ALU_OPS_PER_NODE[name] / sec / 1e12
+            achieved = coded_per_step * ops_per_node[name] / sec / 1e12
             peak = 148 * 4 * 32 * sm_max * 1e6 / 1e12
             roof = {"kernel": name, "bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
                     "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note, "peak_src": ALU_PEAK_NOTE,
@@ -440,14 +460,14 @@ def run_ours(args, rank, world, dist):
         nf = min(len(frames), 8)
         rate, dt = oracle_rate(frames[:nf], L, mb, cores)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{nf} of the step's cfg2 frames encode+decode on {cores} threads, one frame per "
-                         f"task ({dt:.1f} s wall, ~{nf * 2.2:.0f} CPU-s)"}
+               "sample": f"{nf} of the step's {args.workload} frames encode+decode on {cores} threads, one frame "
+                         f"per task ({dt:.1f} s wall)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": t_max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int8 x int8 -> int32 (integer-only)", "data": "synthetic",
-        "config": run_config(B, world),
+        "config": run_config(args, world),
         "details": {"lanes_per_gpu": S, "frames_per_launch": B // S, "points_per_frame": npts / B,
                     "voxels_per_frame": nvox / B},
         "enc_fps": enc_fps, "dec_fps": dec_fps, "points_per_s": pts_tot / (t_max_ms / 1e3),
@@ -475,6 +495,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -392,3 +392,22 @@ def test_alternate_kernels_bit_exact(pcc, env):
     r = subprocess.run([sys.executable, "-c", _ALT.format(root=root)], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert "ALT-OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_bench_launch_configuration_sampled(pcc):
+    """BASELINE.json full size in the launch configuration bench.py times (cfg2, 64 frames
+    per codec launch, C = H = 32): sampled bitstreams byte-identical to the oracle, and
+    every frame of the batch decodes to its unique voxels in Morton order."""
+    from paper_2603_25260_b200.pcc import Codec
+    mb, om = model_pair(32)
+    frames = I.make_frames(I.CFG2, 64, first=0, scene_seed=1)
+    offs = np.cumsum([0] + [len(f) for f in frames]).tolist()
+    codec = Codec(mb, 0)
+    out, oo = codec.encode_frames(dev(np.concatenate(frames)), offs, 12)
+    xyz, no = codec.decode_frames(out, oo, offs[-1])
+    host = out[:oo[-1]].cpu().numpy().tobytes()
+    for i in (0, 37, 63):
+        assert host[oo[i]:oo[i + 1]] == O.encode(om, frames[i], 12), i
+    dec = xyz[:no[-1]].cpu().numpy()
+    for i in range(64):
+        assert np.array_equal(dec[no[i]:no[i + 1]], morton_sorted_unique(frames[i], 12)), i
