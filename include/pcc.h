@@ -82,6 +82,18 @@ size_t pcc_encode_bound(size_t n, int bit_depth);
 pcc_status pcc_build_octree(pcc_ctx c, const int32_t* d_xyz, size_t n, int bit_depth,
                             uint8_t* d_codes, size_t codes_cap, uint32_t* h_level_counts);
 
+/* HRCS statistic (Fig.1c: "(i) the total number of nodes at each level, and
+ * (ii) the average number of occupied neighbors within a 3x3x3 neighborhood"; SPEC
+ * hrcs_stats S:158-166).  `frames` frames concatenated in d_xyz (device int32 [n][3]);
+ * offs is a HOST array of frames+1 point offsets; every frame non-empty (EMPTY),
+ * coordinates < 2^bit_depth (RANGE), bit_depth in [1, 21].  Fills the HOST arrays
+ * h_nodes[f*(L+1) + d] = N_d of frame f and h_nbr[f*(L+1) + d] = sum over frame f's
+ * depth-d nodes of the number of occupied coordinates among the node's 26 neighbours
+ * (exact hash membership, frames never see each other); the paper's mean is
+ * h_nbr / h_nodes.  Caller owns all buffers; no partial output on error. */
+pcc_status pcc_hrcs_stats(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int frames, int bit_depth,
+                          uint64_t* h_nodes, uint64_t* h_nbr);
+
 /* Encode one frame: d_xyz device int32 [n][3] -> bitstream at d_out (device,
  * out_cap bytes).  *out_len = bytes written (or required, on CAPACITY). */
 pcc_status pcc_encode(pcc_ctx c, pcc_model m, const int32_t* d_xyz, size_t n, int bit_depth,

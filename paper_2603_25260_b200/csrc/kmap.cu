@@ -80,6 +80,42 @@ __global__ void k_kmap(const uint64_t* __restrict__ keys, uint32_t n, int depth,
   nbr[t] = r;
 }
 
+// HRCS statistic (Fig.1c; SPEC hrcs_stats S:158-166): per node, the number of
+// occupied coordinates among its 26 neighbours at the same depth (exact hash membership).
+// Per-frame sums: the frame id sits above bit 3d of the key, and lanes of a warp holding
+// the same frame add their counts with one redux + one 64-bit atomic.
+__global__ void k_hrcs(const uint64_t* __restrict__ keys, uint32_t n, int depth, const unsigned long long* __restrict__ tk,
+                       uint64_t mask, uint32_t frame0, unsigned long long* __restrict__ sum) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < n;
+  const uint64_t k = live ? keys[i] : 0ull;
+  const int sh = 3 * depth;
+  const uint64_t fr = sh >= 64 ? 0ull : (k >> sh) << sh;
+  const uint64_t m = k & (sh >= 64 ? ~0ull : ((1ull << sh) - 1ull));
+  const int64_t lim = int64_t(1) << depth;
+  const int64_t X0 = compact3(m >> 2), Y0 = compact3(m >> 1), Z0 = compact3(m);
+  uint32_t cnt = 0;
+  if (live)
+    for (int dl = 0; dl < 27; ++dl) {
+      if (dl == 13) continue;  // the node itself
+      const int64_t X = X0 + dl / 9 - 1, Y = Y0 + (dl / 3) % 3 - 1, Z = Z0 + dl % 3 - 1;
+      if (X < 0 || Y < 0 || Z < 0 || X >= lim || Y >= lim || Z >= lim) continue;
+      const uint64_t q = fr | spread3(uint32_t(X)) << 2 | spread3(uint32_t(Y)) << 1 | spread3(uint32_t(Z));
+      uint64_t h = mix64(q) & mask;
+      while (true) {
+        const unsigned long long s = tk[h];
+        if (s == q) { ++cnt; break; }
+        if (s == EMPTY) break;
+        h = (h + 1) & mask;
+      }
+    }
+  const uint32_t f = live ? uint32_t(sh >= 64 ? 0ull : (k >> sh)) : 0xffffffffu;
+  const uint32_t grp = __match_any_sync(0xffffffffu, f);
+  const uint32_t tot = __reduce_add_sync(grp, cnt);
+  if (live && (threadIdx.x & 31) == uint32_t(__ffs(grp) - 1) && tot)
+    atomicAdd(&sum[f - frame0], (unsigned long long)tot);
+}
+
 }  // namespace
 
 void kernel_map(pcc_ctx c, const uint64_t* keys, uint32_t N, int depth, int32_t* nbr) {
@@ -97,6 +133,25 @@ void kernel_map(pcc_ctx c, const uint64_t* keys, uint32_t N, int depth, int32_t*
   {
     Prof p(c, "kmap", size_t(N) * (8 + 27 * 4));
     k_kmap<<<unsigned((t + 255) / 256), 256, 0, c->stream>>>(keys, N, depth, tk, tv, cap - 1, nbr);
+  }
+  launched(c, 2);
+}
+
+void hrcs_counts(pcc_ctx c, const uint64_t* keys, uint32_t N, int depth, int B, unsigned long long* d_sum) {
+  PCC_CUDA(cudaMemsetAsync(d_sum, 0, size_t(B) * sizeof(unsigned long long), c->stream));
+  if (N == 0) return;
+  uint64_t cap = 1;
+  while (cap < 2ull * N) cap <<= 1;
+  unsigned long long* tk = wsT<unsigned long long>(c, "hash_k", cap);
+  uint32_t* tv = wsT<uint32_t>(c, "hash_v", cap);
+  PCC_CUDA(cudaMemsetAsync(tk, 0xff, cap * sizeof(unsigned long long), c->stream));
+  {
+    Prof p(c, "hrcs", size_t(N) * 8 + cap * 12);
+    k_hash_insert<<<(N + 255) / 256, 256, 0, c->stream>>>(keys, N, tk, tv, cap - 1);
+  }
+  {
+    Prof p(c, "hrcs", size_t(N) * 8);
+    k_hrcs<<<(N + 255) / 256, 256, 0, c->stream>>>(keys, N, depth, tk, cap - 1, 0u, d_sum);
   }
   launched(c, 2);
 }

@@ -176,6 +176,8 @@ void build_octree(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int B, in
 uint32_t expand_level(pcc_ctx c, int d, int B, OctreeOut& o, uint32_t max_nodes);
 // Morton-decode depth-L keys of all frames into xyz (frame bits dropped).
 void keys_to_xyz(pcc_ctx c, const uint64_t* keys, size_t n, int L, int32_t* xyz);
+// HRCS: d_sum[f] = sum over frame f's depth-d nodes of occupied 26-neighbours.
+void hrcs_counts(pcc_ctx c, const uint64_t* keys, uint32_t N, int depth, int B, unsigned long long* d_sum);
 
 // ---- kmap.cu ----
 // nbr[N][27] for the N nodes of one depth (keys include frame bits); absent -> N.

@@ -231,7 +231,7 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
     m->min_depth = int(r.u32());
     m->max_depth = int(r.u32());
     const int C = m->C, H = m->H;
-    if (!(C == 8 || C == 16 || C == 32) || H != C || m->n_deep != 4 || m->R < 1 || m->max_depth > MAX_DEPTH ||
+    if (!(C == 8 || C == 16 || C == 32) || H != C || m->n_deep < 1 || m->n_deep > 4 || m->R < 1 || m->max_depth > MAX_DEPTH ||
         m->min_depth < m->R + 1 + m->n_deep || m->max_depth < m->min_depth)
       throw Error{PCC_ERR_INVALID_ARG};
     r.pos = 40;
@@ -1018,6 +1018,43 @@ pcc_status pcc_build_octree(pcc_ctx c, const int32_t* d_xyz, size_t n, int bit_d
         if (d >= 1) dbg_copy(c, nm("par", d), static_cast<uint32_t*>(c->bufs.at("par").p) + o.nb[d], size_t(o.N[d]) * 4);
       }
     PCC_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+// HRCS statistic: octree of the batch, then per depth one hash build + one
+// 26-probe counting pass (kmap.cu k_hrcs).  Batches split like encode (frame bits).
+pcc_status pcc_hrcs_stats(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int frames, int bit_depth,
+                          uint64_t* h_nodes, uint64_t* h_nbr) {
+  if (!c || !offs || frames < 1 || !h_nodes || !h_nbr) return PCC_ERR_INVALID_ARG;
+  return guard(c, [&] {
+    if (bit_depth < 1 || bit_depth > MAX_DEPTH) throw Error{PCC_ERR_UNSUPPORTED_DEPTH};
+    for (int f = 0; f < frames; ++f) {
+      if (offs[f + 1] < offs[f]) throw Error{PCC_ERR_INVALID_ARG};
+      if (offs[f + 1] == offs[f]) throw Error{PCC_ERR_EMPTY};
+    }
+    if (!d_xyz) throw Error{PCC_ERR_INVALID_ARG};
+    PCC_CUDA(cudaSetDevice(c->device));
+    const int L = bit_depth, fb_max = 64 - 3 * L;
+    const int chunk = fb_max >= 30 ? frames : std::max(1, std::min(frames, 1 << fb_max));
+    std::vector<uint64_t> res(size_t(chunk) * (L + 1));
+    std::vector<size_t> sub;
+    for (int f0 = 0; f0 < frames; f0 += chunk) {
+      const int B = std::min(chunk, frames - f0);
+      sub.assign(offs + f0, offs + f0 + B + 1);
+      for (auto& v : sub) v -= offs[f0];
+      OctreeOut o;
+      build_octree(c, d_xyz + 3 * offs[f0], sub.data(), B, L, o);
+      unsigned long long* d_sum = buf<unsigned long long>(c, "hrcs_sum", size_t(B) * (L + 1));
+      for (int d = 0; d <= L; ++d)
+        hrcs_counts(c, static_cast<uint64_t*>(c->bufs.at("key").p) + o.nb[d], o.N[d], d, B, d_sum + size_t(d) * B);
+      PCC_CUDA(cudaMemcpyAsync(res.data(), d_sum, size_t(B) * (L + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+      PCC_CUDA(cudaStreamSynchronize(c->stream));
+      for (int f = 0; f < B; ++f)
+        for (int d = 0; d <= L; ++d) {
+          h_nodes[size_t(f0 + f) * (L + 1) + d] = o.foff[size_t(d) * (B + 1) + f + 1] - o.foff[size_t(d) * (B + 1) + f];
+          h_nbr[size_t(f0 + f) * (L + 1) + d] = res[size_t(d) * B + f];
+        }
+    }
   });
 }
 

@@ -44,6 +44,7 @@ def _load():
     L.pcc_encode_bound.argtypes = [S, I]
     L.pcc_encode_bound.restype = S
     L.pcc_build_octree.argtypes = [P, P, S, I, P, S, ct.POINTER(ct.c_uint32)]
+    L.pcc_hrcs_stats.argtypes = [P, P, SP, I, I, ct.POINTER(U64), ct.POINTER(U64)]
     L.pcc_encode.argtypes = [P, P, P, S, I, P, S, SP]
     L.pcc_decode.argtypes = [P, P, P, S, P, S, SP, ct.POINTER(I)]
     L.pcc_encode_batch.argtypes = [P, P, P, SP, I, I, P, S, SP]
@@ -64,7 +65,7 @@ def _load():
     L.pcc_debug_gemm_i8.restype = I
     L.pcc_status_string.argtypes = [I]
     L.pcc_status_string.restype = ct.c_char_p
-    for f in ("pcc_model_load", "pcc_model_hash", "pcc_model_info", "pcc_ctx_create", "pcc_build_octree",
+    for f in ("pcc_model_load", "pcc_model_hash", "pcc_model_info", "pcc_ctx_create", "pcc_build_octree", "pcc_hrcs_stats",
               "pcc_encode", "pcc_decode", "pcc_encode_batch", "pcc_decode_batch", "pcc_encode_batch_host",
               "pcc_decode_batch_host", "pcc_debug_tensor", "pcc_ctx_set_debug"):
         getattr(L, f).restype = I
@@ -74,7 +75,7 @@ def _load():
 lib = _load()
 
 EXPORTS = ("pcc_model_load", "pcc_model_hash", "pcc_model_info", "pcc_model_destroy", "pcc_ctx_create",
-           "pcc_ctx_destroy", "pcc_encode_bound", "pcc_build_octree", "pcc_encode", "pcc_decode",
+           "pcc_ctx_destroy", "pcc_encode_bound", "pcc_build_octree", "pcc_hrcs_stats", "pcc_encode", "pcc_decode",
            "pcc_encode_batch", "pcc_decode_batch", "pcc_encode_batch_host", "pcc_decode_batch_host",
            "pcc_debug_tensor", "pcc_ctx_set_debug", "pcc_ctx_launch_count", "pcc_ctx_set_profile",
            "pcc_ctx_profile_get", "pcc_ctx_profile_categories", "pcc_debug_gemm_i8", "pcc_status_string")
@@ -147,6 +148,17 @@ def pcc_build_octree(ctx, d_xyz, n: int, bit_depth: int, d_codes=None, codes_cap
     counts = (ct.c_uint32 * (bit_depth + 1))()
     _chk(lib.pcc_build_octree(ctx, _ptr(d_xyz), n, bit_depth, _ptr(d_codes), codes_cap, counts), "pcc_build_octree")
     return list(counts)
+
+
+def pcc_hrcs_stats(ctx, d_xyz, offs: Sequence[int], bit_depth: int):
+    """Per frame and depth: (node counts, summed occupied 26-neighbours), numpy u64 [frames][L+1]."""
+    frames = len(offs) - 1
+    nodes = (ct.c_uint64 * (frames * (bit_depth + 1)))()
+    nbr = (ct.c_uint64 * (frames * (bit_depth + 1)))()
+    _chk(lib.pcc_hrcs_stats(ctx, _ptr(d_xyz), _sizes(offs), frames, bit_depth, nodes, nbr), "pcc_hrcs_stats")
+    import numpy as np
+    shape = (frames, bit_depth + 1)
+    return (np.frombuffer(nodes, np.uint64).reshape(shape).copy(), np.frombuffer(nbr, np.uint64).reshape(shape).copy())
 
 
 def pcc_encode(ctx, model, d_xyz, n: int, bit_depth: int, d_out, out_cap: int) -> int:

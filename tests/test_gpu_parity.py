@@ -223,6 +223,63 @@ def test_batch_bitstreams_match_oracle(pcc, ctx, cfg, C, B):
         assert np.array_equal(x, morton_sorted_unique(f, sc.bit_depth))
 
 
+@pytest.mark.parametrize("L", [11, 12, 13, 14, 15, 16])
+def test_precision_sweep_matches_oracle(pcc, ctx, L):
+    """NEXT-1 precision sweep (Table 3 averages over 11-16 bit): the 16-beam
+    sensor quantised at L bits, C = 32 GRED+XFP model, bit-identical to the oracle."""
+    import dataclasses
+    sc = dataclasses.replace(I.CFG1, bit_depth=L)
+    mb, om = model_pair(32)
+    m = gpu_model(pcc, mb)
+    frames = I.make_frames(sc, 2, first=5)
+    got, _ = gpu_encode(pcc, ctx, m, frames, L)
+    for f, g in zip(frames, got):
+        assert g == O.encode(om, f, L)
+    dec = gpu_decode(pcc, ctx, m, got, sum(len(f) for f in frames))
+    for f, x in zip(frames, dec):
+        assert np.array_equal(x, morton_sorted_unique(f, L))
+
+
+@pytest.mark.parametrize("n_deep,C", [(3, 32), (3, 8), (2, 32), (1, 16)])
+def test_deep_level_variants_match_oracle(pcc, ctx, n_deep, C):
+    """NEXT-1 t = L-3 variant (n_deep = 3) and shallower splits: the level partition
+    moves, every kernel is reused, the bitstream stays bit-identical."""
+    mb = I.make_model(C=C, H=C, seed=7, n_deep=n_deep, min_depth=9, max_depth=16).to_bytes()
+    om = O.Model(mb)
+    m = gpu_model(pcc, mb)
+    frames = I.make_frames(I.CFG1, 2, first=2)
+    got, _ = gpu_encode(pcc, ctx, m, frames, 12)
+    for f, g in zip(frames, got):
+        assert g[8] == n_deep and g == O.encode(om, f, 12)
+    dec = gpu_decode(pcc, ctx, m, got, sum(len(f) for f in frames))
+    for f, x in zip(frames, dec):
+        assert np.array_equal(x, morton_sorted_unique(f, 12))
+
+
+@pytest.mark.parametrize("case", ["cfg1x3", "cfg2", "cube", "single_L21", "cfg3"])
+def test_hrcs_stats_match_oracle(pcc, ctx, case):
+    """NEXT-3 HRCS statistic: per frame and depth, node count and summed
+    occupied 26-neighbours, exact (integer) against the numpy set-membership oracle."""
+    from oracle import hrcs as OH
+    if case == "cfg1x3":
+        frames, L = I.make_frames(I.CFG1, 3, first=1), 12
+    elif case == "cfg2":
+        frames, L = [I.make_frame(I.CFG2, 2)], 12
+    elif case == "cfg3":
+        frames, L = [I.make_frame(I.CFG3, 1)], 18
+    elif case == "cube":
+        g = np.arange(6, dtype=np.int32)
+        frames, L = [np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3) + 17], 9
+    else:
+        frames, L = [np.array([[7, (1 << 21) - 1, 0]], np.int32), I.random_cloud(800, 21, 3, spread=0.01)], 21
+    offs = np.cumsum([0] + [len(f) for f in frames]).tolist()
+    nodes, nsum = pcc.pcc_hrcs_stats(ctx, dev(np.concatenate(frames).astype(np.int32)), offs, L)
+    for i, f in enumerate(frames):
+        wn, ws = OH.hrcs_stats(f, L)
+        assert nodes[i].tolist() == wn.tolist(), i
+        assert nsum[i].tolist() == ws.tolist(), i
+
+
 def test_batch_equals_single_and_deterministic(pcc, ctx):
     mb, om = model_pair(8)
     m = gpu_model(pcc, mb)

@@ -102,6 +102,25 @@ def test_max_depth_21_round_trip():
     assert L == 21 and _sets_equal(out, pts)
 
 
+@pytest.mark.parametrize("n_deep,L", [(1, 9), (2, 11), (3, 12), (3, 14)])
+def test_deep_level_variants_round_trip(n_deep, L):
+    """NEXT-1 variants: t = L - n_deep + 1 (paper t = L-4 is n_deep = 4; the t = L-3
+    ablation of P:681-710 is n_deep = 3).  The deep/shallow split moves, the container
+    records n_deep, and decode(encode(x)) is still dedup(x) in Morton order."""
+    m = O.Model(I.make_model(C=8, H=8, seed=11, n_deep=n_deep, min_depth=max(R + 1 + n_deep, 9),
+                             max_depth=16).to_bytes())
+    pts = I.random_cloud(2500, L, 4)
+    bs = O.encode(m, pts, L)
+    assert bs[8] == n_deep
+    out, Lo = O.decode(m, bs)
+    assert Lo == L and [tuple(p) for p in out.tolist()] == _morton_sorted(pts, L)
+    # a stream coded with another n_deep is refused before any entropy decoding (S:681)
+    other = O.Model(I.make_model(C=8, H=8, seed=11, n_deep=4 if n_deep != 4 else 3, min_depth=9,
+                                 max_depth=16).to_bytes())
+    with pytest.raises(O.OracleError):
+        O.decode(other, bs)
+
+
 def test_zero_model_closed_form_length():
     m = O.Model(_small_model("zero").to_bytes())
     pts = I.make_frame(I.CFG1)
