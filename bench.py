@@ -37,14 +37,32 @@ WORKLOADS = {  # name -> (channels C = H, description)
     "cfg3": (32, "cfg3: Ford-shaped 64-beam 18-bit LiDAR frames (synthetic ray-cast), L=18, C=H=32 GRED+XFP int8 model"),
     "cfg1": (8, "cfg1: 16-beam x 512 LiDAR frames (synthetic ray-cast), L=12, C=H=8 int8 model"),
 }
+# NEXT-1: the cfg2 sensor at L = 11..16 bits (Table 3 averages over 11-16 bit,
+# P:644) and the t = L-3 variant (n_deep = 3): config-only reuse of every kernel
+for _L in range(11, 17):
+    WORKLOADS[f"cfg2_L{_L}"] = (32, f"cfg2 sensor quantised at L={_L} (precision sweep), C=H=32 GRED+XFP int8 model")
+WORKLOADS["cfg2_t3"] = (32, "cfg2 with the t = L-3 variant (3 deep levels), L=12, C=H=32 GRED+XFP int8 model")
 WORKLOAD = WORKLOADS["cfg2"][1]
 
 
 def workload(args):
     """(ScanConfig, C, description) of --workload."""
+    import dataclasses
     from paper_2603_25260_b200 import inputs as I
     C, desc = WORKLOADS[args.workload]
-    return I.CONFIGS[args.workload], C, desc
+    name = args.workload
+    if name.startswith("cfg2_L"):
+        return dataclasses.replace(I.CFG2, bit_depth=int(name[6:])), C, desc
+    if name == "cfg2_t3":
+        return I.CFG2, C, desc
+    return I.CONFIGS[name], C, desc
+
+
+def model_bytes(args, C):
+    """The seeded random int8 model of --workload (n_deep = 3 for the t = L-3 variant)."""
+    from paper_2603_25260_b200 import inputs as I
+    nd = 3 if args.workload == "cfg2_t3" else 4
+    return I.make_model(C=C, H=C, seed=1, n_deep=nd, min_depth=9, max_depth=18).to_bytes()
 
 
 def peaks():
@@ -153,7 +171,7 @@ def run_reference(args, rank, world):
         return
     from paper_2603_25260_b200 import inputs as I
     cfg, C, _ = workload(args)
-    mb = I.make_model(C=C, H=C, seed=1, min_depth=9, max_depth=18).to_bytes()
+    mb = model_bytes(args, C)
     cores = max(1, min(os.cpu_count() or 1, 8))
     frames, _ = make_inputs(cfg, cores, 0)
     for _ in range(args.warmup):
@@ -250,7 +268,7 @@ def run_ours(args, rank, world, dist):
     L = cfg.bit_depth
     B = args.batch
     S = max(1, min(args.streams, B))
-    mb = I.make_model(C=C, H=C, seed=1, min_depth=9, max_depth=18).to_bytes()
+    mb = model_bytes(args, C)
     frames, offs = make_inputs(cfg, B, shard_frames(rank, world, B)[0])
     npts = offs[-1]
     host_xyz = torch.from_numpy(np.concatenate(frames).astype(np.int32)).pin_memory()

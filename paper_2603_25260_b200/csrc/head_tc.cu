@@ -10,9 +10,10 @@
 //      and run the softmax over the row with 16-column tcgen05.ld loads: pass 1 requantises z to Q8 logits (written
 //      back with tcgen05.st) and finds max / first argmax, pass 2 turns them into LUT
 //      exponentials (written back) and their sum S, pass 3 forms p = 1 + floor(e*65281/S)
-//      (exact: 64-bit reciprocal + one integer correction) and either the (cum, freq)
-//      of the true symbol (encoder) or the cumulative row (decoder, staged in smem and
-//      written with coalesced stores).
+//      (exact: 32-bit reciprocal + one integer correction) and either the (cum, freq)
+//      of the true symbol (encoder) or the cumulative row (decoder: p back into TMEM,
+//      quarter totals exchanged, then the row staged in smem and copied out coalesced; the leftover is
+//      carried as row meta in entry 255 and applied by the rANS decoder).
 // Bit-exact with the oracle's cdf_quantize / head_logits (integer arithmetic only).
 #include "pcc_internal.cuh"
 #include "rq.cuh"
@@ -86,8 +87,7 @@ struct SmemLayout {
   static constexpr int RED = MBAR + 16;          // [4][128] x (a, b) int32 = 4 KB
   static constexpr int ROWI = RED + 4096;        // [128] x 8 int32 = 4 KB
   static constexpr int STAGE = ROWI + 4096;      // decoder: 128 x STG u16 (66 KB)
-  static constexpr int MASK = STAGE + TILE * STG * 2;  // decoder: [9][4] u32 leftover masks
-  static constexpr int FST = MASK + 9 * 16;      // the tile's input rows F, prefetched by cp.async (<= 8 KB)
+  static constexpr int FST = STAGE + TILE * STG * 2;  // the tile's input rows F, prefetched by cp.async (<= 8 KB)
   static constexpr int END = FST + TILE * 64;
 };
 
@@ -113,7 +113,6 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   uint32_t* thold = reinterpret_cast<uint32_t*>(sm + S::THOLD);
   int32_t* red = reinterpret_cast<int32_t*>(sm + S::RED);    // red[(q*128 + r)*2 + {0,1}]
   int32_t* rowi = reinterpret_cast<int32_t*>(sm + S::ROWI);  // rowi[r*8 + k]
-  uint16_t* stage = reinterpret_cast<uint16_t*>(sm + S::STAGE);
   const int tid = threadIdx.x, warp = tid >> 5;
   const int r = 32 * (warp & 3) + (tid & 31);  // row of the tile (= TMEM lane)
   const int q = warp >> 2;                     // column quarter
@@ -133,10 +132,6 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   for (int k = tid; k < 256; k += NT) sb2[k] = b2[k];
   for (int k = tid; k < H * CW; k += NT) sW1[k] = reinterpret_cast<const int32_t*>(W1)[k];
   for (int k = tid; k < H; k += NT) sb1[k] = b1[k];
-  if (MODE == 1 && tid < 36) {  // MASK[t][u]: halves of word u (chunk elements 2u, 2u+1) with index >= t
-    const int t = tid >> 2, u = tid & 3;
-    reinterpret_cast<uint32_t*>(sm + S::MASK)[tid] = (2 * u >= t ? 0x0000ffffu : 0u) | (2 * u + 1 >= t ? 0xffff0000u : 0u);
-  }
   if (warp == 0) tc::tmem_alloc<256>(thold);
   if (tid == 0) tc::mbar_init(mbar, 1);
   tc::fence_async_smem();
@@ -172,11 +167,11 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
   auto hidden_and_bias = [&](uint32_t tl) {
     const uint32_t rw = tl * TILE + r;
     const bool vr = rw < n;
+    uint32_t ab[2] = {0u, 0u};
+    int32_t hacc[HQ];
     int32_t fw[CW];
 #pragma unroll
     for (int w = 0; w < CW; ++w) fw[w] = vr ? reinterpret_cast<const int32_t*>(sm + S::FST + r * C)[w] : 0;
-    uint32_t ab[2] = {0u, 0u};
-    int32_t hacc[HQ];
 #pragma unroll
     for (int hh = 0; hh < HQ; ++hh) {
       const int h = q * HQ + hh;
@@ -341,10 +336,11 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       if (s32) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          // t = e*65281 - (q_est + 1) S = remainder - S in [-S, S): q = q_est + (t >= 0)
+          // t = e*65281 - (q_est + 1) S = remainder - S in [-S, S): q = q_est + (t >= 0),
+          // p = 1 + q = q_est + 2 + (t >> 31, arithmetic: -1 when t < 0)
           const uint32_t qt = __umulhi(v[k], inv32);
           const uint32_t t = v[k] * 65281u + qt * nS + nS;
-          v[k] = qt + 1u + (~t >> 31);
+          v[k] = qt + 2u + uint32_t(int32_t(t) >> 31);
         }
       } else {
 #pragma unroll
@@ -399,8 +395,10 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         cf[row] = cm | (f << 16);
       }
     } else {
-      uint16_t* srow = stage + r * STG;
-      uint32_t run = 0;
+      // decoder row format (DESIGN.md §5 "CDF rows"): entries 0..254 = cum_i = sum_{j<i} p_j
+      // WITHOUT the leftover, entry 255 = istar | left << 8 (left in [0, 255)); the rANS
+      // decoder applies the leftover.  3a: p and the quarter total (p back into TMEM);
+      // 3b: quarter prefix + cumulative row, written from registers (16-byte stores).
 #pragma unroll 1
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t v[16];
@@ -408,61 +406,47 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
         tc::tmem_wait_ld();
         pchunk(v);
 #pragma unroll
-        for (int k8 = 0; k8 < 16; k8 += 8) {  // 8 entries -> one 16-byte shared store
-          uint32_t w[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t c0 = run;  // quarter-local prefix (< 2^16)
-            run += v[k8 + 2 * u];
-            w[u] = (c0 & 0xffffu) | (run << 16);
-            run += v[k8 + 2 * u + 1];
-          }
-          *reinterpret_cast<uint4*>(srow + 64 * q + ch * 16 + k8) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
+        for (int k = 0; k < 16; k += 2) tot += v[k] + v[k + 1];
+        tmem_st16(taddr + ch * 16, v);
       }
-      if (q == 3) run -= 1u;  // padding column 255
+      if (q == 3) tot -= 1u;  // padding column 255 (e = 0 -> p = 1)
       HEAD_TRACE(4, tr0);
-      bar_rows();  // Ssum reads done
-      red[(q * TILE + r) * 2] = int32_t(run);
+      bar_rows();  // Ssum / istar reads done
+      red[(q * TILE + r) * 2] = int32_t(tot);
+      tmem_wait_st();
       bar_rows();
-      if (q == 0) {
-        uint32_t o = 0;
-        for (int qq = 0; qq < 4; ++qq) {
-          rowi[r * 8 + qq] = int32_t(o);  // prefix of the quarter totals
-          o += uint32_t(red[(qq * TILE + r) * 2]);
+      const uint32_t t0 = uint32_t(red[r * 2]), t1 = uint32_t(red[(TILE + r) * 2]), t2 = uint32_t(red[(2 * TILE + r) * 2]),
+                     t3 = uint32_t(red[(3 * TILE + r) * 2]);
+      uint32_t run = (q > 0 ? t0 : 0u) + (q > 1 ? t1 : 0u) + (q > 2 ? t2 : 0u);
+      const uint32_t meta = uint32_t(istar) | ((65536u - (t0 + t1 + t2 + t3)) << 8);
+      uint16_t* srow = reinterpret_cast<uint16_t*>(sm + S::STAGE) + r * STG + 64 * q;
+#pragma unroll 1
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t v[16];
+        tmem_ld16(taddr + ch * 16, v);
+        tc::tmem_wait_ld();
+        uint32_t w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t c0 = run;
+          run += v[2 * u];
+          w[u] = __byte_perm(c0, run, 0x5410);
+          run += v[2 * u + 1];
         }
-        rowi[r * 8 + 4] = int32_t(65536u - o);  // leftover
-        rowi[r * 8 + 5] = istar;
+        if (q == 3 && ch == 3) w[7] = __byte_perm(w[7], meta, 0x5410);  // index 255: row meta
+        *reinterpret_cast<uint4*>(srow + 16 * ch) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(srow + 16 * ch + 8) = make_uint4(w[4], w[5], w[6], w[7]);
       }
       bar_rows();
-      // coalesced write-out: 16 rows per iteration, 32 threads x 16 bytes per 512-byte row.
-      // Packed u16 pairs: every cdf value below index 255 is < 2^16, so the quarter offset
-      // and the leftover are added to both halves at once without carries; the leftover
-      // goes to the elements after the first argmax: t = how many of the chunk's 8
-      // elements are <= istar selects the half-word mask of each word.
+      // coalesced copy-out: a warp writes whole 512-byte rows (32 lanes x 16 B) of its lane
+      // quarter's rows (32 (w % 4) + w / 4 + 4 i), staged by the same 128 threads
       const uint32_t rows_here = (n - tile * TILE) < uint32_t(TILE) ? (n - tile * TILE) : uint32_t(TILE);
-      // rows of this warp's lane quarter only (32 * (w % 4) + w / 4 + 4 i): staged by the
-      // same 128 threads, so the row barrier suffices
-      const uint32_t j = uint32_t(tid) & 31u, sub = 32u * uint32_t(warp & 3) + uint32_t(warp >> 2), jq = j >> 3;
-      const uint4* mask4 = reinterpret_cast<const uint4*>(sm + S::MASK);
-      const uint16_t* sp = stage + sub * STG + 8 * j;
-      const int32_t* rp = rowi + sub * 8;
+      const uint32_t j = uint32_t(tid) & 31u, sub = 32u * uint32_t(warp & 3) + uint32_t(warp >> 2);
+      const uint16_t* sp = reinterpret_cast<const uint16_t*>(sm + S::STAGE) + sub * STG + 8 * j;
       uint4* gp = reinterpret_cast<uint4*>(cdf + (size_t(tile) * TILE + sub) * 256) + j;
       const uint32_t rend = min(rows_here, 32u * uint32_t(warp & 3) + 32u);
-      for (uint32_t rr = sub; rr < rend; rr += 4, sp += 4 * STG, rp += 4 * 8, gp += 4 * 32) {
-        const uint32_t offw = uint32_t(rp[jq]) * 0x10001u;
-        const int2 li = *reinterpret_cast<const int2*>(rp + 4);  // leftover, first argmax
-        const uint32_t leftw = uint32_t(li.x) * 0x10001u;
-        const uint4 m = mask4[min(max(li.y + 1 - int(8 * j), 0), 8)];
-        const uint4 g = *reinterpret_cast<const uint4*>(sp);
-        uint4 o;
-        o.x = g.x + offw + (leftw & m.x);
-        o.y = g.y + offw + (leftw & m.y);
-        o.z = g.z + offw + (leftw & m.z);
-        o.w = g.w + offw + (leftw & m.w);
-        if (j == 31u) o.w = (o.w & 0xffffu) | 0xffff0000u;  // index 255: padding
-        *gp = o;
-      }
+#pragma unroll 2
+      for (uint32_t rr = sub; rr < rend; rr += 4, sp += 4 * STG, gp += 4 * 32) *gp = *reinterpret_cast<const uint4*>(sp);
     }
     HEAD_TRACE(5, tr0);
     // next tile: its F rows landed (own copies + row barrier), hidden layer into A and the

@@ -318,10 +318,10 @@ __global__ void __launch_bounds__(256) k_head_cdf(const int8_t* __restrict__ F, 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
     const uint32_t left = 65536u - ps;
-#pragma unroll
-    for (int t = 0; t < 8; ++t)
-      if (8 * lane + t == ist) p[t] += left;
     if constexpr (MODE == 0) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (8 * lane + t == ist) p[t] += left;
       const int sym = int(X[node]) - 1;
       uint32_t cum = 0, fq = 0;
 #pragma unroll
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(256) k_head_cdf(const int8_t* __restrict__ F, 
         run += p[t];
         uint32_t c1 = run;
         run += p[t + 1];
-        if (8 * lane + t + 1 >= NCODE) c1 = 0xffffu;
+        if (8 * lane + t + 1 >= NCODE) c1 = uint32_t(ist) | (left << 8);  // row meta
         h[t / 2] = (c0 & 0xffffu) | (c1 << 16);
       }
       *reinterpret_cast<uint4*>(cdf + size_t(node) * 256 + 8 * lane) = make_uint4(h[0], h[1], h[2], h[3]);
