@@ -479,7 +479,11 @@ std::vector<int32_t> head_logits(const Head& h, const Feat& F, size_t n, int C, 
 // l_i = clamp(round(z_i * m_l / 2^r_l), -2^24, 2^24)  (Q8 logits, 1/256 nat)
 // delta_i = max_k l_k - l_i >= 0  ("numerically stable form", "non-positive domain")
 // e_i = delta_i < 4096 ? LUT[delta_i >> 2] : 0   (LUT[j] = round(2^24 exp(-j/64)))
-// S = sum e_i;  p_i = 1 + floor(e_i * 65281 / S);  p_{i*} += 65536 - sum p  (i* = first argmax)
+// S = sum e_i ("accumulation ... 32-bit integer arithmetic");
+// normalisation (reading Q21, revised): cumulative floors of the prefix sums
+//   E_i = sum_{j<i} e_j,  C_i = i + floor(E_i * 65281 / S)  (i = 0..255),
+//   p_i = C_{i+1} - C_i,
+// so C_0 = 0, C_255 = 255 + 65281 = 65536 exactly, and every p_i >= 1.
 void cdf_quantize(const int32_t* z, const RQ& rql, const std::vector<uint32_t>& lut, uint32_t* p) {
   int64_t l[NCODE];
   for (int i = 0; i < NCODE; ++i) {
@@ -490,24 +494,21 @@ void cdf_quantize(const int32_t* z, const RQ& rql, const std::vector<uint32_t>& 
     l[i] = v;
   }
   int64_t mu = l[0];
-  int istar = 0;
   for (int i = 1; i < NCODE; ++i)
-    if (l[i] > mu) {
-      mu = l[i];
-      istar = i;
-    }
+    if (l[i] > mu) mu = l[i];
   uint64_t e[NCODE], S = 0;
   for (int i = 0; i < NCODE; ++i) {
     int64_t dl = mu - l[i];
     e[i] = dl < 4096 ? uint64_t(lut[size_t(dl >> 2)]) : 0u;
     S += e[i];
   }
-  uint64_t tot = 0;
+  uint64_t E = 0, C = 0;  // E_0 = 0, C_0 = 0
   for (int i = 0; i < NCODE; ++i) {
-    p[i] = uint32_t(1u + (e[i] * 65281u) / S);
-    tot += p[i];
+    E += e[i];
+    const uint64_t Cn = uint64_t(i + 1) + (E * 65281u) / S;  // C_{i+1}
+    p[i] = uint32_t(Cn - C);
+    C = Cn;
   }
-  p[istar] += uint32_t(65536u - tot);
 }
 
 // ---- rANS (reading O9/O10/Q23/Q24) ---------------------------------------------

@@ -2,10 +2,11 @@
 
 Pins (DESIGN.md §"Oracle pins"):
 * LUT entries vs math.exp (the LUT is data written by the model generator);
-* closed forms (tests/golden/cdf_closed_forms.json): all-equal logits and a
-  logit >= 16 nats above the rest;
-* invariants on random rows: sum p = 65536, min p >= 1, monotone in the logit,
-  invariant to a common shift, equivariant to permutation;
+* closed forms (tests/golden/cdf_closed_forms.json): all-equal logits, a logit >= 16
+  nats above the rest, two equal maxima >= 16 nats above the rest;
+* invariants on random rows: sum p = 65536, min p >= 1, invariant to a common shift;
+  each p_i is 1 + floor or 1 + ceil of e_i 65281 / S (a difference of two floors,
+  reading Q21), hence monotone in the logit up to one count;
 * the derived approximation bound |p_i/2^16 - softmax_i| <= 0.012*softmax_i + 0.0040
   (LUT step e^{3/256}-1 < 0.0118 relative; normalisation <= 256/65536 absolute);
 * rANS: decode(encode(s)) = s; code length within the entropy bound of the
@@ -37,12 +38,19 @@ def test_lut_against_math_exp():
 def test_closed_forms():
     g = {c["name"]: c for c in json.load(open(GOLD))["cases"]}
     p = O.cdf(np.full((1, 255), 12345, np.int32), 1, 0, LUT)[0]
-    assert p[0] == g["all_equal"]["p_first"] and np.all(p[1:] == g["all_equal"]["p_rest"])
+    assert p[254] == g["all_equal"]["p_last"] and np.all(p[:254] == g["all_equal"]["p_rest"])
     for pos in (0, 17, 254):
         z = np.zeros((1, 255), np.int32)
         z[0, pos] = g["dominant"]["gap_q8"]
         p = O.cdf(z, 1, 0, LUT)[0]
         assert p[pos] == g["dominant"]["p_max"] and np.all(np.delete(p, pos) == g["dominant"]["p_rest"])
+    t = g["two_maxima"]
+    for a, b in ((0, 1), (3, 200), (100, 254)):
+        z = np.zeros((1, 255), np.int32)
+        z[0, a] = z[0, b] = t["gap_q8"]
+        p = O.cdf(z, 1, 0, LUT)[0]
+        assert p[a] == t["p_first_max"] and p[b] == t["p_second_max"]
+        assert np.all(np.delete(p, [a, b]) == t["p_rest"])
 
 
 def _softmax_q8(z):
@@ -60,21 +68,32 @@ def test_invariants_and_bound():
         q = _softmax_q8(z)
         err = np.abs(p / 65536.0 - q)
         assert np.all(err <= 0.012 * q + 0.0040), err.max()
-        # monotone: l_i >= l_j  ->  p_i >= p_j
+        # p_i - 1 is floor(E_{i+1} K/S) - floor(E_i K/S), i.e. floor or ceil of e_i K/S:
+        # checked against exact rationals from the model's LUT exponentials
+        l = z.astype(np.int64)  # m = 1, r = 0: Q8 logits are z itself (|z| < 2^24)
+        d = l.max(1, keepdims=True) - l
+        e = np.where(d < 4096, LUT[np.minimum(d, 4095) >> 2].astype(np.int64), 0)
+        S = e.sum(1, keepdims=True)
+        lo, hi = 1 + (e * 65281) // S, 1 + -((-e * 65281) // S)
+        assert np.all((p == lo) | (p == hi))
+        # hence monotone in the logit up to one count: l_i >= l_j -> p_i >= p_j - 1
         for r in range(0, 2000, 97):
             o = np.argsort(z[r], kind="stable")
-            assert np.all(np.diff(p[r][o]) >= 0)
+            assert np.all(np.diff(p[r][o]) >= -1)
 
 
-def test_shift_and_permutation():
+def test_shift_and_cumulative_structure():
     rng = np.random.default_rng(12)
     z = rng.normal(0, 1000, size=(200, 255)).astype(np.int32)
     p = O.cdf(z, 1, 0, LUT)
     assert np.array_equal(O.cdf(z + 77777, 1, 0, LUT), p)
-    perm = rng.permutation(255)
-    # equivariance holds whenever the max is unique (the leftover goes to the argmax)
-    uniq = (z == z.max(1, keepdims=True)).sum(1) == 1
-    assert np.array_equal(O.cdf(z[:, perm], 1, 0, LUT)[uniq], p[:, perm][uniq])
+    # splitting the row at any symbol: the cumulative count before it is the floor of its
+    # exact share of the prefix mass, i.e. within one count of 65536 * (prefix softmax mass)
+    cum = np.concatenate([np.zeros((200, 1), np.int64), np.cumsum(p.astype(np.int64), 1)], 1)
+    q = _softmax_q8(z)
+    qc = np.concatenate([np.zeros((200, 1)), np.cumsum(q, 1)], 1)
+    i = np.arange(256)[None, :]
+    assert np.all(np.abs(cum - i - 65281 * qc) <= 1 + 0.012 * 65281 * qc + 1e-6)
 
 
 def test_logit_requant_clamp():

@@ -2,7 +2,7 @@
 
 Pins (DESIGN.md §"Oracle pins"):
 * decode(encode(x)) == dedup(x) in Morton order (SPEC S:705; north_star);
-* zero model: every pmf is [258, 257 x 254] (closed form), so the payload length is
+* zero model: every pmf is [257 x 254, 258] (closed form), so the payload length is
   fixed by the code histogram alone, within the rANS bound (words <= 1.002*ideal
   + 16K bits; >= 0.98*ideal - 32: the integer state update x' = (x//f)*M + x%f + c
   has a zero-mean deviation from x*M/f whose Jensen gap makes the words ~0.5 %
@@ -127,8 +127,8 @@ def test_zero_model_closed_form_length():
     keys, codes = O.build_octree(pts, 12)
     L, levels = _parse(O.encode(m, pts, 12))
     for d in range(R, L):
-        n1 = int((codes[d] == 1).sum())
-        ideal = n1 * math.log2(65536 / 258) + (codes[d].size - n1) * math.log2(65536 / 257)
+        n255 = int((codes[d] == 255).sum())  # symbol 255 = index 254 gets 258 (reading Q21)
+        ideal = n255 * math.log2(65536 / 258) + (codes[d].size - n255) * math.log2(65536 / 257)
         bits, K = _payload_bits(levels[d], codes[d].size)
         assert ideal * 0.98 - 16 * K - 16 <= bits <= ideal * 1.002 + 16 * K, d
 
