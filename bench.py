@@ -239,11 +239,13 @@ def aggregate(allst, K):
 ALU_PEAK_NOTE = ("B200 integer issue peak = 148 SM x 4 SMSP x 32 lanes x 1 instr/clk x sm_max clock "
                  "(DESIGN.md §5)")
 # Algorithmic integer ops per coded node of the predictor + integer softmax:
-# hidden layer C*H/4 dp4a (C = H = 32) + 12 ops per symbol (logit requant mul-add, shift,
-# saturate; max; delta; LUT index/load/select; sum; scale multiply; quotient; correction;
-# accumulate) x 255; the decoder adds the prefix-sum store (13 per symbol).
+# hidden layer C*H/4 dp4a (C = H = 32) + 9 ops per symbol for the exponentials (logit
+# requant mul-add, shift, saturate; max; delta; LUT index/load/select; sum); reading Q21's
+# cumulative floors then cost the encoder one prefix add per symbol and two exact 64-bit
+# divisions per node (~10 ops each), the decoder per symbol a prefix add, scale multiply,
+# quotient, correction, index add and the store (15 per symbol in all).
 def alu_ops_per_node(C, H):
-    return {"head_enc": C * H / 4 + 12 * 255, "head_dec": C * H / 4 + 13 * 255}
+    return {"head_enc": C * H / 4 + 10 * 255 + 20, "head_dec": C * H / 4 + 15 * 255}
 
 
 def measured_traffic(kernel: str):

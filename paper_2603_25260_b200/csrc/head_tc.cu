@@ -7,13 +7,15 @@
 //   2. z = a W2^T: ONE tcgen05.mma.kind::i8 (M = 128, N = 256, K = 32) into TMEM
 //      (int32; column 255 is padding);
 //   3. four threads own TMEM lane r = node r of the tile (one 64-column quarter each)
-//      and run the softmax over the row with 16-column tcgen05.ld loads: pass 1 requantises z to Q8 logits (written
-//      back with tcgen05.st) and finds max / first argmax, pass 2 turns them into LUT
-//      exponentials (written back) and their sum S, pass 3 forms p = 1 + floor(e*65281/S)
-//      (exact: 32-bit reciprocal + one integer correction) and either the (cum, freq)
-//      of the true symbol (encoder) or the cumulative row (decoder: p back into TMEM,
-//      quarter totals exchanged, then the row staged in smem and copied out coalesced; the leftover is
-//      carried as row meta in entry 255 and applied by the rANS decoder).
+//      and run the softmax over the row with 16-column tcgen05.ld loads: pass 1 finds
+//      max z (the logit requant is monotone), pass 2 turns the logits into LUT
+//      exponentials and the quarter sums of e; the normalisation is reading Q21's
+//      cumulative floors C_i = i + floor(E_i * 65281 / S) (E_i = prefix sum of e):
+//      the encoder needs only C_sym and C_{sym+1} (prefix mass before the true symbol
+//      from pass 2, two exact divisions per node), the decoder writes the whole row
+//      C_0..C_254 (pass 3: e back from TMEM, one exact division per entry: 32-bit
+//      reciprocal estimate + a sign-bit remainder test), staged in smem and copied out
+//      as whole 512-byte rows.
 // Bit-exact with the oracle's cdf_quantize / head_logits (integer arithmetic only).
 #include "pcc_internal.cuh"
 #include "rq.cuh"
@@ -264,10 +266,11 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     // the whole row avoids saturation: l = low word of the 64-bit shift, no selects
     const bool nosat = !SAT || (zmx <= zsat_hi && zmn >= zsat_lo);
     HEAD_TRACE(2, tr0);
-    // ---- pass 2: Q8 logit, e = LUT[delta >> 2] (0 beyond 16 nats), local sum and
-    //      local first index with delta == 0 (e stored back into TMEM) ----
-    uint32_t ssum = 0;
-    uint32_t kmin = 0xffffffffu;  // min over (min(delta, 4096) << 8) + i: the first i with delta == 0
+    // ---- pass 2: Q8 logit, e = LUT[delta >> 2] (0 beyond 16 nats) and the quarter sum;
+    //      decoder: e stored back into TMEM; encoder: the prefix mass before the true
+    //      symbol and its own e (reading Q21: C_i = i + floor(E_i * 65281 / S)) ----
+    const int sym = (MODE == 0 && valid) ? int(X[row]) - 1 : 0;
+    uint32_t ssum = 0, pre = 0, es = 0;
     const int64_t lm = rql.mp;
     const int lr = rql.r;
     // one-multiply form (rq.cuh, signed): delta = mu - lq(z) = hi32(z * (-M) + mu 2^32 + 2^31 - 1)
@@ -279,14 +282,11 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       uint32_t v[16];
       tmem_ld16(taddr + ch * 16, v);
       tc::tmem_wait_ld();
-      uint32_t kc = 0xffffffffu;
       if (fastl) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const uint32_t dl = uint32_t(int32_t((int64_t(int32_t(v[k])) * nM + C2) >> 32));
-          const uint32_t dc = min(dl, 4096u);
-          kc = min(kc, (dc << 8) + uint32_t(k));
-          v[k] = sLut[dc];  // LUT4[4096] = 0: delta >= 4096
+          v[k] = sLut[min(dl, 4096u)];  // LUT4[4096] = 0: delta >= 4096
         }
       } else {
 #pragma unroll
@@ -299,144 +299,91 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
             lv = zz > zsat_hi ? (1 << 24) : lv;
             lv = zz < zsat_lo ? -(1 << 24) : lv;
           }
-          const uint32_t dc = min(uint32_t(mu - lv), 4096u);
-          kc = min(kc, (dc << 8) + uint32_t(k));
-          v[k] = sLut[dc];
+          v[k] = sLut[min(uint32_t(mu - lv), 4096u)];
         }
       }
-      kmin = min(kmin, kc + uint32_t(64 * q + ch * 16));
       if (q == 3 && ch == 3) v[15] = 0u;  // column 255 is padding, not a symbol
+      uint32_t cs16 = 0;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) ssum += v[k];
-      tmem_st16(taddr + ch * 16, v);
-    }
-    const int ist = int(kmin < 256u ? kmin : (1u << 30));
-    bar_rows();  // everyone has read red (pass-1 values) before it is overwritten
-    red[(q * TILE + r) * 2] = int32_t(ssum);
-    red[(q * TILE + r) * 2 + 1] = ist;
-    bar_rows();
-    const uint32_t Ssum = uint32_t(red[r * 2]) + uint32_t(red[(TILE + r) * 2]) + uint32_t(red[(2 * TILE + r) * 2]) +
-                          uint32_t(red[(3 * TILE + r) * 2]);
-    const int istar = min(min(red[r * 2 + 1], red[(TILE + r) * 2 + 1]),
-                          min(red[(2 * TILE + r) * 2 + 1], red[(3 * TILE + r) * 2 + 1]));
-    tmem_wait_st();
-    HEAD_TRACE(3, tr0);
-    // ---- pass 3: p = 1 + floor(e * 65281 / S) (exact), leftover to the first argmax ----
-    // q = floor(e * 65281 / S): estimate with the 32-bit reciprocal inv32 =
-    // floor(65281 * 2^32 / S) (< 2^24 since S >= LUT[0] = 2^24), q_est in {q - 1, q},
-    // then one exact 64-bit correction.
-    const uint32_t inv32 = uint32_t((65281ull << 32) / uint64_t(Ssum));
-    // S <= 2^31: the remainder r = e*65281 - q_est*S lies in [0, 2S) subset [0, 2^32), so
-    // the correction is exact in 32-bit wrap-around arithmetic; otherwise use 64 bits.
-    const bool s32 = Ssum <= 0x80000000u;
-    const uint32_t nS = 0u - Ssum;
-    // p = 1 + q for the 16 exponentials of a chunk (the s32 choice is per row, hoisted
-    // out of the element loop so only one variant is issued)
-    auto pchunk = [&](uint32_t (&v)[16]) {
-      if (s32) {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          // t = e*65281 - (q_est + 1) S = remainder - S in [-S, S): q = q_est + (t >= 0),
-          // p = 1 + q = q_est + 2 + (t >> 31, arithmetic: -1 when t < 0)
-          const uint32_t qt = __umulhi(v[k], inv32);
-          const uint32_t t = v[k] * 65281u + qt * nS + nS;
-          v[k] = qt + 2u + uint32_t(int32_t(t) >> 31);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const uint32_t qt = __umulhi(v[k], inv32);
-          v[k] = 1u + qt + ((uint64_t(v[k]) * 65281ull - uint64_t(qt) * Ssum) >= uint64_t(Ssum) ? 1u : 0u);
-        }
-      }
-    };
-    uint32_t tot = 0;
-    if constexpr (MODE == 0) {
-      const int sym = valid ? int(X[row]) - 1 : 0;
-      uint32_t cum = 0, fq = 0;
-#pragma unroll 1
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t v[16];
-        tmem_ld16(taddr + ch * 16, v);
-        tc::tmem_wait_ld();
-        pchunk(v);
-        uint32_t cs16 = 0;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) cs16 += v[k];
-        tot += cs16;
+      for (int k = 0; k < 16; ++k) cs16 += v[k];
+      ssum += cs16;
+      if constexpr (MODE == 0) {
         const int i0 = 64 * q + ch * 16;
         if (sym >= i0 + 16) {
-          cum += cs16;  // the whole chunk precedes the symbol
+          pre += cs16;  // the whole chunk precedes the symbol
         } else if (sym >= i0) {  // the chunk holding the symbol (one per row)
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
-            cum += (i0 + k < sym) ? v[k] : 0u;
-            fq = (i0 + k == sym) ? v[k] : fq;
+            pre += (i0 + k < sym) ? v[k] : 0u;
+            es = (i0 + k == sym) ? v[k] : es;
           }
         }
-      }
-      if (q == 3) tot -= 1u;  // the padding column 255 (e = 0 -> p = 1) is not a symbol
-      HEAD_TRACE(4, tr0);
-      bar_rows();  // Ssum reads done
-      red[(q * TILE + r) * 2] = int32_t(tot);
-      rowi[r * 8 + q] = int32_t(cum);
-      rowi[r * 8 + 4 + q] = int32_t(fq);
-      bar_rows();
-      if (q == 0 && valid) {
-        uint32_t T = 0, cm = 0, f = 0;
-        for (int qq = 0; qq < 4; ++qq) {
-          T += uint32_t(red[(qq * TILE + r) * 2]);
-          cm += uint32_t(rowi[r * 8 + qq]);
-          f += uint32_t(rowi[r * 8 + 4 + qq]);
-        }
-        const uint32_t left = 65536u - T;
-        if (istar < sym) cm += left;
-        if (istar == sym) f += left;
-        cf[row] = cm | (f << 16);
-      }
-    } else {
-      // decoder row format (DESIGN.md §5 "CDF rows"): entries 0..254 = cum_i = sum_{j<i} p_j
-      // WITHOUT the leftover, entry 255 = istar | left << 8 (left in [0, 255)); the rANS
-      // decoder applies the leftover.  3a: p and the quarter total (p back into TMEM);
-      // 3b: quarter prefix + cumulative row, written from registers (16-byte stores).
-#pragma unroll 1
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t v[16];
-        tmem_ld16(taddr + ch * 16, v);
-        tc::tmem_wait_ld();
-        pchunk(v);
-#pragma unroll
-        for (int k = 0; k < 16; k += 2) tot += v[k] + v[k + 1];
+      } else {
         tmem_st16(taddr + ch * 16, v);
       }
-      if (q == 3) tot -= 1u;  // padding column 255 (e = 0 -> p = 1)
+    }
+    bar_rows();  // everyone has read red (pass-1 values) before it is overwritten
+    red[(q * TILE + r) * 2] = int32_t(ssum);
+    red[(q * TILE + r) * 2 + 1] = int32_t(pre);
+    if (MODE == 0) rowi[r * 8 + q] = int32_t(es);
+    bar_rows();
+    const uint32_t s0 = uint32_t(red[r * 2]), s1 = uint32_t(red[(TILE + r) * 2]), s2 = uint32_t(red[(2 * TILE + r) * 2]),
+                   s3 = uint32_t(red[(3 * TILE + r) * 2]);
+    const uint32_t Ssum = s0 + s1 + s2 + s3;  // <= 255 * 2^24 < 2^32
+    HEAD_TRACE(3, tr0);
+    if constexpr (MODE == 0) {
+      // encoder: (cum, freq) = (C_sym, C_{sym+1} - C_sym), two exact divisions per node
+      if (q == 0 && valid) {
+        const uint64_t E = uint64_t(uint32_t(red[r * 2 + 1])) + uint32_t(red[(TILE + r) * 2 + 1]) +
+                           uint32_t(red[(2 * TILE + r) * 2 + 1]) + uint32_t(red[(3 * TILE + r) * 2 + 1]);
+        const uint64_t e1 = uint64_t(uint32_t(rowi[r * 8])) + uint32_t(rowi[r * 8 + 1]) + uint32_t(rowi[r * 8 + 2]) +
+                            uint32_t(rowi[r * 8 + 3]);
+        const uint32_t c0 = uint32_t(sym) + uint32_t((E * 65281ull) / Ssum);
+        const uint32_t c1 = uint32_t(sym) + 1u + uint32_t(((E + e1) * 65281ull) / Ssum);
+        cf[row] = c0 | ((c1 - c0) << 16);
+      }
       HEAD_TRACE(4, tr0);
-      bar_rows();  // Ssum / istar reads done
-      red[(q * TILE + r) * 2] = int32_t(tot);
+    } else {
+      // decoder: the cumulative row C_0..C_254 (entry 255 = C_255 = 65536 is implicit),
+      // one exact division per entry: q_est = umulhi(E, inv32) with inv32 =
+      // floor(65281 * 2^32 / S) is q or q - 1 (E <= S < 2^32); for S <= 2^31 the test
+      // t = E*65281 - (q_est + 1) S (in [-S, S), exact mod 2^32) decides, else 64 bits.
       tmem_wait_st();
-      bar_rows();
-      const uint32_t t0 = uint32_t(red[r * 2]), t1 = uint32_t(red[(TILE + r) * 2]), t2 = uint32_t(red[(2 * TILE + r) * 2]),
-                     t3 = uint32_t(red[(3 * TILE + r) * 2]);
-      uint32_t run = (q > 0 ? t0 : 0u) + (q > 1 ? t1 : 0u) + (q > 2 ? t2 : 0u);
-      const uint32_t meta = uint32_t(istar) | ((65536u - (t0 + t1 + t2 + t3)) << 8);
+      const uint32_t inv32 = uint32_t((65281ull << 32) / uint64_t(Ssum));
+      const bool s32 = Ssum <= 0x80000000u;
+      const uint32_t nS = 0u - Ssum;
+      uint32_t E = (q > 0 ? s0 : 0u) + (q > 1 ? s1 : 0u) + (q > 2 ? s2 : 0u);  // mass before this quarter
       uint16_t* srow = reinterpret_cast<uint16_t*>(sm + S::STAGE) + r * STG + 64 * q;
 #pragma unroll 1
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t v[16];
         tmem_ld16(taddr + ch * 16, v);
         tc::tmem_wait_ld();
+        uint32_t c[16];
+        if (s32) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const uint32_t qt = __umulhi(E, inv32);
+            const uint32_t t = E * 65281u + qt * nS + nS;
+            c[k] = qt + uint32_t(64 * q + 16 * ch + k + 1) + uint32_t(int32_t(t) >> 31);  // i + floor(E K / S)
+            E += v[k];
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const uint32_t qt = __umulhi(E, inv32);
+            const uint32_t qq = qt + ((uint64_t(E) * 65281ull - uint64_t(qt) * Ssum) >= uint64_t(Ssum) ? 1u : 0u);
+            c[k] = qq + uint32_t(64 * q + 16 * ch + k);
+            E += v[k];
+          }
+        }
         uint32_t w[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t c0 = run;
-          run += v[2 * u];
-          w[u] = __byte_perm(c0, run, 0x5410);
-          run += v[2 * u + 1];
-        }
-        if (q == 3 && ch == 3) w[7] = __byte_perm(w[7], meta, 0x5410);  // index 255: row meta
+        for (int u = 0; u < 8; ++u) w[u] = __byte_perm(c[2 * u], c[2 * u + 1], 0x5410);
         *reinterpret_cast<uint4*>(srow + 16 * ch) = make_uint4(w[0], w[1], w[2], w[3]);
         *reinterpret_cast<uint4*>(srow + 16 * ch + 8) = make_uint4(w[4], w[5], w[6], w[7]);
       }
+      HEAD_TRACE(4, tr0);
       bar_rows();
       // coalesced copy-out: a warp writes whole 512-byte rows (32 lanes x 16 B) of its lane
       // quarter's rows (32 (w % 4) + w / 4 + 4 i), staged by the same 128 threads

@@ -266,7 +266,6 @@ __global__ void __launch_bounds__(256) k_head_cdf(const int8_t* __restrict__ F, 
     // logits z_i and Q8 requant l_i = clamp(round(z m / 2^r), +-2^24)
     int32_t l[8];
     int32_t lmax = INT32_MIN;
-    int imax = 1 << 30;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const int i = 8 * lane + t;
@@ -277,20 +276,10 @@ __global__ void __launch_bounds__(256) k_head_cdf(const int8_t* __restrict__ F, 
       if (rql.r > 0) v = (v + (int64_t(1) << (rql.r - 1))) >> rql.r;
       v = v < -(int64_t(1) << 24) ? -(int64_t(1) << 24) : (v > (int64_t(1) << 24) ? (int64_t(1) << 24) : v);
       l[t] = int32_t(v);
-      if (i < NCODE && l[t] > lmax) {
-        lmax = l[t];
-        imax = i;
-      }
+      if (i < NCODE) lmax = max(lmax, l[t]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-    int ist = 1 << 30;  // first argmax
-#pragma unroll
-    for (int t = 0; t < 8; ++t)
-      if (8 * lane + t < NCODE && l[t] == lmax) { ist = 8 * lane + t; break; }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ist = min(ist, __shfl_xor_sync(0xffffffffu, ist, o));
-    (void)imax;
     // e_i = LUT[delta >> 2] (0 beyond 16 nats), S = sum e
     uint32_t e[8];
     uint32_t s = 0;
@@ -302,59 +291,44 @@ __global__ void __launch_bounds__(256) k_head_cdf(const int8_t* __restrict__ F, 
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    // p_i = 1 + floor(e_i * 65281 / S): reciprocal inv = floor((2^64-1)/S) then one
-    // exact integer correction (q* - q in {0,1}).
-    const uint64_t inv = ~0ull / uint64_t(s);
-    uint32_t p[8];
-    uint32_t ps = 0;
+    // reading Q21: C_i = i + floor(E_i * 65281 / S), E_i = sum_{j<i} e_j (exact: reciprocal
+    // inv = floor((2^64-1)/S), then one integer correction)
+    uint32_t ls = 0;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const uint64_t num = uint64_t(e[t]) * 65281ull;
+    for (int t = 0; t < 8; ++t) ls += e[t];
+    uint32_t inc = ls;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    const uint64_t inv = ~0ull / uint64_t(s);
+    auto Cq = [&](uint32_t E, int i) -> uint32_t {  // C_i for prefix mass E
+      const uint64_t num = uint64_t(E) * 65281ull;
       uint64_t qq = __umul64hi(num, inv);
       if (num - qq * uint64_t(s) >= uint64_t(s)) ++qq;
-      p[t] = (8 * lane + t < NCODE) ? uint32_t(1 + qq) : 0u;
-      ps += p[t];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-    const uint32_t left = 65536u - ps;
+      return uint32_t(i) + uint32_t(qq);
+    };
+    uint32_t E = inc - ls;  // mass before this lane's symbols
     if constexpr (MODE == 0) {
-#pragma unroll
-      for (int t = 0; t < 8; ++t)
-        if (8 * lane + t == ist) p[t] += left;
       const int sym = int(X[node]) - 1;
-      uint32_t cum = 0, fq = 0;
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const int i = 8 * lane + t;
-        if (i < sym) cum += p[t];
-        if (i == sym) fq = p[t];
+        if (i == sym) {
+          const uint32_t c0 = Cq(E, i), c1 = Cq(E + e[t], i + 1);
+          cf[node] = c0 | ((c1 - c0) << 16);
+        }
+        E += e[t];
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        cum += __shfl_xor_sync(0xffffffffu, cum, o);
-        fq += __shfl_xor_sync(0xffffffffu, fq, o);
-      }
-      if (lane == 0) cf[node] = cum | (fq << 16);
     } else {
-      uint32_t tot = 0;
-#pragma unroll
-      for (int t = 0; t < 8; ++t) tot += p[t];
-      uint32_t inc = tot;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-      }
-      uint32_t run = inc - tot;
       uint32_t h[4];
 #pragma unroll
       for (int t = 0; t < 8; t += 2) {
-        const uint32_t c0 = run;
-        run += p[t];
-        uint32_t c1 = run;
-        run += p[t + 1];
-        if (8 * lane + t + 1 >= NCODE) c1 = uint32_t(ist) | (left << 8);  // row meta
+        const uint32_t c0 = Cq(E, 8 * lane + t);
+        E += e[t];
+        const uint32_t c1 = Cq(E, 8 * lane + t + 1);  // index 255 (lane 31): C_255 = 65536 -> 0, unused
+        E += e[t + 1];
         h[t / 2] = (c0 & 0xffffu) | (c1 << 16);
       }
       *reinterpret_cast<uint4*>(cdf + size_t(node) * 256 + 8 * lane) = make_uint4(h[0], h[1], h[2], h[3]);

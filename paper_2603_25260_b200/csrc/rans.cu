@@ -130,26 +130,17 @@ __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs
     if (act) {
       const uint16_t* c = rows + size_t(s % DEC_STAGES) * stage_rows * 256 + lane * 256;
       const uint32_t slot = x & 0xffffu;
-      // row: c[0..254] = cumulative p WITHOUT the leftover, c[255] = istar | left << 8
-      // (head_tc.cu); the true cum'_i = c[i] + left [i > istar], f'_istar = p_istar + left.
-      // Slots inside istar's widened interval map to c[istar], later ones move down by left.
-      const uint32_t meta = c[255];
-      const int ist = int(meta & 0xffu);
-      const uint32_t left = meta >> 8;
-      const uint32_t tot = 65536u - left;  // c[255] of a plain cumulative row
-      const uint32_t c_is = c[ist];
-      const uint32_t n_is = ist < NCODE - 1 ? uint32_t(c[ist + 1]) : tot;
-      const uint32_t sl = slot < c_is ? slot : (slot < n_is + left ? c_is : slot - left);
+      // row: c[i] = C_i (reading Q21), C_0 = 0, C_255 = 65536 implicit (entry 255 unused)
       int lo = 0, hi = NCODE - 1;
 #pragma unroll
       for (int it = 0; it < 8; ++it) {
         const int mid = (lo + hi + 1) >> 1;
         if (lo < hi) {
-          if (uint32_t(c[mid]) <= sl) lo = mid; else hi = mid - 1;
+          if (uint32_t(c[mid]) <= slot) lo = mid; else hi = mid - 1;
         }
       }
-      const uint32_t cum = uint32_t(c[lo]) + (lo > ist ? left : 0u);
-      const uint32_t nxt = (lo < NCODE - 1 ? uint32_t(c[lo + 1]) : tot) + (lo >= ist ? left : 0u);
+      const uint32_t cum = c[lo];
+      const uint32_t nxt = lo < NCODE - 1 ? uint32_t(c[lo + 1]) : 65536u;
       const uint32_t f = nxt - cum;
       X[sg.node + j] = uint8_t(lo + 1);
       x = f * (x >> 16) + slot - cum;

@@ -196,16 +196,8 @@ def test_decoder_cdf_parity(pcc, ctx):
             p = D.get(f"p/{d}", np.uint16).reshape(-1, 255).astype(np.int64)
             cum = np.concatenate([np.zeros((p.shape[0], 1), np.int64), np.cumsum(p, 1)[:, :254]], 1)
             got = np.frombuffer(pcc.pcc_debug_tensor(ctx, f"cdf/{d}"), np.uint16).reshape(-1, 256).astype(np.int64)
-            # row format: c[0..254] cumulative without the leftover,
-            # c[255] = istar | left << 8; the decoder's cum'_i = c[i] + left [i > istar]
-            ist, left = got[:, 255] & 0xFF, got[:, 255] >> 8
-            assert (ist < 255).all() and (left < 255).all(), d
-            idx = np.arange(255)[None, :]
-            full = got[:, :255] + left[:, None] * (idx > ist[:, None])
-            assert np.array_equal(full, cum), d
-            # with a positive leftover, istar is the first argmax of the oracle's pmf
-            pos = left > 0
-            assert np.array_equal(ist[pos], np.argmax(p, 1)[pos]), d
+            # row format: c[i] = C_i for i = 0..254, entry 255 unused
+            assert np.array_equal(got[:, :255], cum), d
             assert np.array_equal(np.frombuffer(pcc.pcc_debug_tensor(ctx, f"code/{d}"), np.uint8),
                                   D.get(f"code/{d}", np.uint8)), d
     finally:
