@@ -45,7 +45,6 @@ __device__ unsigned long long g_head_trace[2][8];
 
 constexpr int TILE = 128;
 constexpr uint32_t IDESC = tc::idesc_i8(128, 256);
-constexpr int STG = 264;  // staged cdf row stride in u16 (528 B: 16-B aligned, STS.128/LDS.128 conflict-free)
 
 __device__ __forceinline__ int32_t lq8(int32_t z, RQ q) {  // Q8 logit, clamp +-2^24
   int64_t v = int64_t(z) * int64_t(q.mp);
@@ -76,20 +75,24 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
 // thread t owns row r = 32*(w%4) + t%32 of the tile and column quarter q = w/4
 // (columns 64q..64q+63); the 4 threads of a row combine max / sum / totals in smem.
 constexpr int NT = 512;
+template <int MODE>
 struct SmemLayout {
   static constexpr int B = 0;           // W2 operand 256 x 32 (8 KB)
   static constexpr int A = 8192;        // a operand 128 x 32 (4 KB)
-  // exp table indexed by delta itself: LUT4[j] = LUT[j >> 2] for j < 4096, LUT4[4096] = 0
-  static constexpr int LUT = 12288;              // 4097 x u32 (16 KB + 4 B)
-  static constexpr int B2 = LUT + 16400;         // 1 KB
+  // encoder: exp table indexed by delta itself, LUT4[j] = LUT[j >> 2] for j < 4096,
+  // LUT4[4096] = 0; decoder: the compact table LUT[j >> 2] (1024 + the 0 sentinel), since
+  // it stores j = min(delta, 4096) >> 2 in its rows anyway and needs the smem for them
+  static constexpr int LUT = 12288;
+  static constexpr int LUT_N = MODE == 0 ? 4097 : 1025;
+  static constexpr int B2 = LUT + ((LUT_N * 4 + 15) & ~15);  // 1 KB
   static constexpr int W1 = B2 + 1024;           // <= 1 KB
   static constexpr int B1 = W1 + 1024;           // <= 256 B
   static constexpr int MBAR = B1 + 256;
   static constexpr int THOLD = MBAR + 8;
   static constexpr int RED = MBAR + 16;          // [4][128] x (a, b) int32 = 4 KB
   static constexpr int ROWI = RED + 4096;        // [128] x 8 int32 = 4 KB
-  static constexpr int STAGE = ROWI + 4096;      // decoder: 128 x STG u16 (66 KB)
-  static constexpr int FST = STAGE + TILE * STG * 2;  // the tile's input rows F, prefetched by cp.async (<= 8 KB)
+  static constexpr int STAGE = ROWI + 4096;      // decoder: 128 rows x DROW_BYTES (74 KB)
+  static constexpr int FST = STAGE + (MODE == 1 ? TILE * DROW_BYTES : 0);  // the tile's F rows (cp.async, <= 8 KB)
   static constexpr int END = FST + TILE * 64;
 };
 
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
                                                    uint32_t* __restrict__ cf, uint16_t* __restrict__ cdf,
                                                    int8_t* __restrict__ a_dbg, int32_t zsat_lo, int32_t zsat_hi) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  using S = SmemLayout;
+  using S = SmemLayout<MODE>;
   const int64_t lhalf = rql.r > 0 ? (int64_t(1) << (rql.r - 1)) : 0;
   uint8_t* sB = sm + S::B;
   uint8_t* sA = sm + S::A;
@@ -129,8 +132,13 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     *reinterpret_cast<uint32_t*>(sB + tc::kmaj_off(rr, 4 * w)) = v;
   }
   for (int k = tid; k < 1024; k += NT) reinterpret_cast<uint32_t*>(sA)[k] = 0u;  // K padding stays 0
-  for (int k = tid; k < 4096; k += NT) sLut[k] = lut[k >> 2];
-  if (tid == 0) sLut[4096] = 0u;  // delta >= 4096 (16 nats): e = 0 (reading Q20)
+  if constexpr (MODE == 0) {
+    for (int k = tid; k < 4096; k += NT) sLut[k] = lut[k >> 2];
+    if (tid == 0) sLut[4096] = 0u;  // delta >= 4096 (16 nats): e = 0 (reading Q20)
+  } else {
+    for (int k = tid; k < 1024; k += NT) sLut[k] = lut[k];
+    if (tid == 0) sLut[1024] = 0u;
+  }
   for (int k = tid; k < 256; k += NT) sb2[k] = b2[k];
   for (int k = tid; k < H * CW; k += NT) sW1[k] = reinterpret_cast<const int32_t*>(W1)[k];
   for (int k = tid; k < H; k += NT) sb1[k] = b1[k];
@@ -277,12 +285,44 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     const bool fastl = rql.fast_s && nosat;
     const int32_t nM = -rql.Sp;
     const int64_t C2 = (int64_t(mu) << 32) + 0x7fffffff;
+    uint32_t csum[4];  // decoder: the quarter's chunk sums (prefix mass at 16-symbol blocks)
+    uint8_t* jrow = sm + S::STAGE + r * DROW_BYTES + DROW_HDR + 128 * q;  // decoder: this quarter's j
 #pragma unroll 1
     for (int ch = 0; ch < 4; ++ch) {
       uint32_t v[16];
       tmem_ld16(taddr + ch * 16, v);
       tc::tmem_wait_ld();
-      if (fastl) {
+      if (MODE == 1 && fastl) {
+        // decoder row entry j = min(delta, 4096) >> 2 (the model LUT index, 1024: e = 0)
+        uint32_t jw[8];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const uint32_t dl = uint32_t(int32_t((int64_t(int32_t(v[k])) * nM + C2) >> 32));
+          const uint32_t jj = min(dl, 4096u) >> 2;
+          if (k & 1) jw[k >> 1] = __byte_perm(jw[k >> 1], jj, 0x5410);
+          else jw[k >> 1] = jj;
+          v[k] = sLut[jj];
+        }
+        *reinterpret_cast<uint4*>(jrow + 32 * ch) = make_uint4(jw[0], jw[1], jw[2], jw[3]);
+        *reinterpret_cast<uint4*>(jrow + 32 * ch + 16) = make_uint4(jw[4], jw[5], jw[6], jw[7]);
+      } else if (MODE == 1) {
+        uint32_t jw[8];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int32_t zz = int32_t(v[k]);
+          int32_t lv = int32_t((int64_t(zz) * lm + lhalf) >> lr);
+          if (SAT && !nosat) {
+            lv = zz > zsat_hi ? (1 << 24) : lv;
+            lv = zz < zsat_lo ? -(1 << 24) : lv;
+          }
+          const uint32_t jj = min(uint32_t(mu - lv), 4096u) >> 2;
+          if (k & 1) jw[k >> 1] = __byte_perm(jw[k >> 1], jj, 0x5410);
+          else jw[k >> 1] = jj;
+          v[k] = sLut[jj];
+        }
+        *reinterpret_cast<uint4*>(jrow + 32 * ch) = make_uint4(jw[0], jw[1], jw[2], jw[3]);
+        *reinterpret_cast<uint4*>(jrow + 32 * ch + 16) = make_uint4(jw[4], jw[5], jw[6], jw[7]);
+      } else if (fastl) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const uint32_t dl = uint32_t(int32_t((int64_t(int32_t(v[k])) * nM + C2) >> 32));
@@ -319,7 +359,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
           }
         }
       } else {
-        tmem_st16(taddr + ch * 16, v);
+        csum[ch] = cs16;
       }
     }
     bar_rows();  // everyone has read red (pass-1 values) before it is overwritten
@@ -344,56 +384,35 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       }
       HEAD_TRACE(4, tr0);
     } else {
-      // decoder: the cumulative row C_0..C_254 (entry 255 = C_255 = 65536 is implicit),
-      // one exact division per entry: q_est = umulhi(E, inv32) with inv32 =
-      // floor(65281 * 2^32 / S) is q or q - 1 (E <= S < 2^32); for S <= 2^31 the test
-      // t = E*65281 - (q_est + 1) S (in [-S, S), exact mod 2^32) decides, else 64 bits.
-      tmem_wait_st();
-      const uint32_t inv32 = uint32_t((65281ull << 32) / uint64_t(Ssum));
-      const bool s32 = Ssum <= 0x80000000u;
-      const uint32_t nS = 0u - Ssum;
+      // decoder row header: S, inv32 = floor(65281 * 2^32 / S), and the prefix mass
+      // E_{16k} before each 16-symbol block (this quarter's blocks k = 4q + ch); the rANS
+      // decoder rebuilds C_i = i + floor(E_i * 65281 / S) where its search needs it
+      uint32_t* hdr = reinterpret_cast<uint32_t*>(sm + S::STAGE + r * DROW_BYTES);
       uint32_t E = (q > 0 ? s0 : 0u) + (q > 1 ? s1 : 0u) + (q > 2 ? s2 : 0u);  // mass before this quarter
-      uint16_t* srow = reinterpret_cast<uint16_t*>(sm + S::STAGE) + r * STG + 64 * q;
-#pragma unroll 1
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t v[16];
-        tmem_ld16(taddr + ch * 16, v);
-        tc::tmem_wait_ld();
-        uint32_t c[16];
-        if (s32) {
+      if (q == 0) {
+        hdr[0] = Ssum;
+        hdr[1] = uint32_t((65281ull << 32) / uint64_t(Ssum));
+      } else {
+        hdr[1 + 4 * q] = E;  // block 4q
+      }
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const uint32_t qt = __umulhi(E, inv32);
-            const uint32_t t = E * 65281u + qt * nS + nS;
-            c[k] = qt + uint32_t(64 * q + 16 * ch + k + 1) + uint32_t(int32_t(t) >> 31);  // i + floor(E K / S)
-            E += v[k];
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const uint32_t qt = __umulhi(E, inv32);
-            const uint32_t qq = qt + ((uint64_t(E) * 65281ull - uint64_t(qt) * Ssum) >= uint64_t(Ssum) ? 1u : 0u);
-            c[k] = qq + uint32_t(64 * q + 16 * ch + k);
-            E += v[k];
-          }
-        }
-        uint32_t w[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) w[u] = __byte_perm(c[2 * u], c[2 * u + 1], 0x5410);
-        *reinterpret_cast<uint4*>(srow + 16 * ch) = make_uint4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<uint4*>(srow + 16 * ch + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+      for (int ch = 0; ch < 3; ++ch) {
+        E += csum[ch];
+        hdr[2 + 4 * q + ch] = E;  // block 4q + ch + 1
       }
       HEAD_TRACE(4, tr0);
       bar_rows();
-      // coalesced copy-out: a warp writes whole 512-byte rows (32 lanes x 16 B) of its lane
-      // quarter's rows (32 (w % 4) + w / 4 + 4 i), staged by the same 128 threads
+      // coalesced copy-out of the lane group's 32 rows (contiguous in global and in smem):
+      // 32 x 37 16-byte chunks over the group's 128 threads
       const uint32_t rows_here = (n - tile * TILE) < uint32_t(TILE) ? (n - tile * TILE) : uint32_t(TILE);
-      const uint32_t j = uint32_t(tid) & 31u, sub = 32u * uint32_t(warp & 3) + uint32_t(warp >> 2);
-      const uint16_t* sp = reinterpret_cast<const uint16_t*>(sm + S::STAGE) + sub * STG + 8 * j;
-      uint4* gp = reinterpret_cast<uint4*>(cdf + (size_t(tile) * TILE + sub) * 256) + j;
-      const uint32_t rend = min(rows_here, 32u * uint32_t(warp & 3) + 32u);
+      const uint32_t g0 = 32u * uint32_t(warp & 3);
+      const uint32_t grow = rows_here > g0 ? min(32u, rows_here - g0) : 0u;
+      constexpr uint32_t RCH16 = DROW_BYTES / 16;
+      const uint4* sp = reinterpret_cast<const uint4*>(sm + S::STAGE + g0 * DROW_BYTES);
+      uint4* gp = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(cdf) + (size_t(tile) * TILE + g0) * DROW_BYTES);
+      const uint32_t gt = uint32_t(warp >> 2) * 32u + (uint32_t(tid) & 31u);  // 0..127 within the group
 #pragma unroll 2
-      for (uint32_t rr = sub; rr < rend; rr += 4, sp += 4 * STG, gp += 4 * 32) *gp = *reinterpret_cast<const uint4*>(sp);
+      for (uint32_t t = gt; t < grow * RCH16; t += 128u) gp[t] = sp[t];
     }
     HEAD_TRACE(5, tr0);
     // next tile: its F rows landed (own copies + row barrier), hidden layer into A and the
@@ -460,12 +479,12 @@ void launch_head(pcc_ctx c, const int8_t* F, uint32_t n, const DHead& L, const u
   auto kern = k_head_tc<C, H, MODE, SAT>;
   static bool attr = false;
   if (!attr) {
-    PCC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemLayout::END));
+    PCC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemLayout<MODE>::END));
     attr = true;
   }
   const uint32_t ntiles = (n + TILE - 1) / TILE;
   const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 2u));
-  kern<<<grid, NT, SmemLayout::END, c->stream>>>(F, n, L.W1, L.b1, L.rq1, L.W2, L.b2, L.rql, lut, X, cf, cdf, a_dbg,
+  kern<<<grid, NT, SmemLayout<MODE>::END, c->stream>>>(F, n, L.W1, L.b1, L.rq1, L.W2, L.b2, L.rql, lut, X, cf, cdf, a_dbg,
                                                  L.zsat_lo, L.zsat_hi);
   launched(c);
 }

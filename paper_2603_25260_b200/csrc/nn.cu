@@ -281,11 +281,12 @@ __global__ void __launch_bounds__(256) k_head_cdf(const int8_t* __restrict__ F, 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
     // e_i = LUT[delta >> 2] (0 beyond 16 nats), S = sum e
-    uint32_t e[8];
+    uint32_t e[8], jv[8];
     uint32_t s = 0;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const uint32_t dl = uint32_t(lmax - l[t]);
+      jv[t] = min(dl, 4096u) >> 2;  // decoder row entry (1024: e = 0)
       e[t] = (8 * lane + t < NCODE && dl < 4096u) ? luts[dl >> 2] : 0u;
       s += e[t];
     }
@@ -322,16 +323,17 @@ __global__ void __launch_bounds__(256) k_head_cdf(const int8_t* __restrict__ F, 
         E += e[t];
       }
     } else {
-      uint32_t h[4];
-#pragma unroll
-      for (int t = 0; t < 8; t += 2) {
-        const uint32_t c0 = Cq(E, 8 * lane + t);
-        E += e[t];
-        const uint32_t c1 = Cq(E, 8 * lane + t + 1);  // index 255 (lane 31): C_255 = 65536 -> 0, unused
-        E += e[t + 1];
-        h[t / 2] = (c0 & 0xffffu) | (c1 << 16);
+      // decoder row (pcc_internal.cuh DROW_*): S, inv32, E_{16k} (k = 1..15), j entries
+      uint8_t* row = reinterpret_cast<uint8_t*>(cdf) + size_t(node) * DROW_BYTES;
+      uint32_t* hdr = reinterpret_cast<uint32_t*>(row);
+      if (lane == 0) {
+        hdr[0] = s;
+        hdr[1] = uint32_t((65281ull << 32) / uint64_t(s));
+      } else if ((lane & 1) == 0) {
+        hdr[1 + lane / 2] = E;  // mass before symbol 8 lane = 16 (lane / 2)
       }
-      *reinterpret_cast<uint4*>(cdf + size_t(node) * 256 + 8 * lane) = make_uint4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<uint4*>(row + DROW_HDR + 16 * lane) =
+          make_uint4(jv[0] | jv[1] << 16, jv[2] | jv[3] << 16, jv[4] | jv[5] << 16, jv[6] | jv[7] << 16);
     }
   }
 }

@@ -231,8 +231,14 @@ struct DecSeg {
   uint32_t level_bytes;
   uint32_t last;     // 1 if this is the level's last segment (must end the payload)
 };
-void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf, uint8_t* X,
-                 uint32_t* err, int max_lanes);
+// Decoder row per node (DESIGN.md §5 "decoder rows", reading Q21): u32 S, u32 inv32 =
+// floor(65281 * 2^32 / S), u32 E_{16k} for k = 1..15 (prefix mass before symbol 16k),
+// 3 u32 pad, then u16 j_i = min(delta_i, 4096) >> 2 for i = 0..254 (1024: e = 0) and one
+// pad entry: 592 bytes (16-byte multiple).  The rANS decoder rebuilds
+// C_i = i + floor(E_i * 65281 / S) only where its search needs it.
+constexpr int DROW_BYTES = 592, DROW_HDR = 80, DROW_U16 = DROW_BYTES / 2;
+void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf,
+                 const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes);
 
 // ---- pack (runtime.cu) ----
 struct PackItem {    // encoder output item: frame header+raw prefix (kind 0) or one segment (kind 1)

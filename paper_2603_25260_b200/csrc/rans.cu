@@ -59,13 +59,17 @@ __device__ __forceinline__ uint32_t ld_u32(const uint8_t* p) {
 // resident CTAs per SM beat deeper prefetch on the bandwidth-bound levels).
 template <int DEC_STAGES>
 __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs, int nseg, const uint8_t* __restrict__ bs,
-                                                 const uint16_t* __restrict__ cdf, uint8_t* __restrict__ X,
-                                                 uint32_t* __restrict__ err, int stage_rows) {
-  extern __shared__ __align__(128) uint16_t rows[];  // [DEC_STAGES][stage_rows][256]
+                                                 const uint16_t* __restrict__ cdf, const uint32_t* __restrict__ lut,
+                                                 uint8_t* __restrict__ X, uint32_t* __restrict__ err, int stage_rows) {
+  extern __shared__ __align__(128) uint16_t rows[];  // [DEC_STAGES][stage_rows][DROW_U16]
   __shared__ __align__(8) uint64_t dec_mbar[DEC_STAGES];
+  __shared__ uint32_t slut[1025];  // the model's exp table, slut[1024] = 0 (delta >= 4096)
   const int gw = blockIdx.x;
   const int lane = threadIdx.x;
   if (gw >= nseg) return;
+  for (int k = lane; k < 1024; k += 32) slut[k] = lut[k];
+  if (lane == 0) slut[1024] = 0u;
+  __syncwarp();
   const DecSeg sg = segs[gw];
   const uint8_t* lvl = bs + sg.byte;
   const uint32_t lvl_bytes = sg.level_bytes;
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs
   uint32_t wbase = 0;  // window = words [wbase, wbase + 96)
   uint32_t w0 = ldw(lane), w1 = ldw(32 + lane), w2 = ldw(64 + lane);
   const uint32_t steps = (n + uint32_t(K) - 1u) / uint32_t(K);
-  const uint16_t* base = cdf + size_t(sg.node) * 256;
+  const uint16_t* base = cdf + size_t(sg.node) * DROW_U16;
   const unsigned lt = (1u << lane) - 1u;
   // The K rows of a step are contiguous (nodes s*K .. s*K+K-1): one TMA bulk copy per
   // step, issued by lane 0, completing on that stage's mbarrier.
@@ -114,8 +118,9 @@ __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs
       const uint32_t j0 = s * uint32_t(K);
       const uint32_t nr = (n - j0) < uint32_t(K) ? (n - j0) : uint32_t(K);
       uint64_t* mb = &dec_mbar[s % DEC_STAGES];
-      tc::mbar_expect_tx(mb, nr * 512u);
-      tc::bulk_g2s(rows + size_t(s % DEC_STAGES) * stage_rows * 256, base + size_t(j0) * 256, nr * 512u, mb);
+      tc::mbar_expect_tx(mb, nr * uint32_t(DROW_BYTES));
+      tc::bulk_g2s(rows + size_t(s % DEC_STAGES) * stage_rows * DROW_U16, base + size_t(j0) * DROW_U16,
+                   nr * uint32_t(DROW_BYTES), mb);
     }
   };
 #pragma unroll
@@ -128,19 +133,49 @@ __global__ void __launch_bounds__(32) k_rans_dec(const DecSeg* __restrict__ segs
     const bool act = lane < K && j < n;
     bool need = false;
     if (act) {
-      const uint16_t* c = rows + size_t(s % DEC_STAGES) * stage_rows * 256 + lane * 256;
+      const uint16_t* rw = rows + size_t(s % DEC_STAGES) * stage_rows * DROW_U16 + lane * DROW_U16;
+      const uint32_t* hd = reinterpret_cast<const uint32_t*>(rw);
+      const uint16_t* jx = rw + DROW_HDR / 2;
       const uint32_t slot = x & 0xffffu;
-      // row: c[i] = C_i (reading Q21), C_0 = 0, C_255 = 65536 implicit (entry 255 unused)
-      int lo = 0, hi = NCODE - 1;
+      const uint32_t S = hd[0], inv32 = hd[1];
+      // C_i <= slot  <=>  i <= slot and E_i * 65281 < (slot - i + 1) * S (exact, 64-bit);
+      // C_i is non-decreasing in i, so the block is the number of true coarse tests
+      const uint64_t sS = uint64_t(S);
+      int blk = 0;
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (lo < hi) {
-          if (uint32_t(c[mid]) <= slot) lo = mid; else hi = mid - 1;
+      for (int k = 1; k < 16; ++k) {
+        const uint32_t i = 16u * uint32_t(k);
+        blk += (i <= slot && uint64_t(hd[1 + k]) * 65281ull < uint64_t(slot - i + 1u) * sS) ? 1 : 0;
+      }
+      // inside the block: its 16 LUT indices in two 16-byte loads, the 16 exponentials as
+      // independent loads, then the running prefix and one exact test per symbol
+      const uint4* jq = reinterpret_cast<const uint4*>(jx + 16 * blk);
+      const uint4 ja = jq[0], jb = jq[1];
+      const uint32_t jw[8] = {ja.x, ja.y, ja.z, ja.w, jb.x, jb.y, jb.z, jb.w};
+      uint32_t ev[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) ev[t] = slut[(jw[t >> 1] >> (16 * (t & 1))) & 0xffffu];
+      const uint32_t E0 = blk ? hd[1 + blk] : 0u;
+      uint32_t Er = E0, Elo = E0, elo = ev[0];
+      int cnt = 0;
+#pragma unroll
+      for (int t = 0; t < 15; ++t) {
+        Er += ev[t];  // E_{16 blk + t + 1}
+        const uint32_t i1 = uint32_t(16 * blk + t + 1);
+        if (i1 < uint32_t(NCODE) && i1 <= slot && uint64_t(Er) * 65281ull < uint64_t(slot - i1 + 1u) * sS) {
+          cnt = t + 1;
+          Elo = Er;
+          elo = ev[t + 1];
         }
       }
-      const uint32_t cum = c[lo];
-      const uint32_t nxt = lo < NCODE - 1 ? uint32_t(c[lo + 1]) : 65536u;
+      const int lo = 16 * blk + cnt;
+      // C_lo and C_{lo+1} exactly: q = floor(E K / S) from the 32-bit reciprocal estimate
+      auto fl = [&](uint32_t Ev) -> uint32_t {
+        const uint32_t qt = __umulhi(Ev, inv32);
+        return qt + ((uint64_t(Ev) * 65281ull - uint64_t(qt) * sS) >= sS ? 1u : 0u);
+      };
+      const uint32_t cum = uint32_t(lo) + fl(Elo);
+      const uint32_t nxt = lo < NCODE - 1 ? uint32_t(lo + 1) + fl(Elo + elo) : 65536u;
       const uint32_t f = nxt - cum;
       X[sg.node + j] = uint8_t(lo + 1);
       x = f * (x >> 16) + slot - cum;
@@ -179,15 +214,15 @@ void rans_encode(pcc_ctx c, const EncSeg* d_segs, int nseg, const uint32_t* cf, 
   launched(c);
 }
 
-void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf, uint8_t* X,
-                 uint32_t* err, int max_lanes) {
+void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf,
+                 const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes) {
   if (nseg == 0) return;
   const int stage_rows = max_lanes <= 8 ? 8 : (max_lanes <= 16 ? 16 : 32);
   static bool attr = false;
   if (!attr) {
-    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 32 * 512));
-    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32 * 512));
-    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 512));
+    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 32 * DROW_BYTES));
+    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32 * DROW_BYTES));
+    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * DROW_BYTES));
     attr = true;
   }
   // two stages: measured best on the B = 256 bench (2.55 ms vs 2.87 / 3.02 ms per step for
@@ -199,11 +234,11 @@ void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, c
     return e ? atoi(e) : 0;
   }();
   if (forced >= 2 && forced <= 4) st = forced;
-  const size_t smem = size_t(st) * stage_rows * 512;
+  const size_t smem = size_t(st) * stage_rows * DROW_BYTES;
   Prof p(c, "rans_dec", 0);
-  if (st == 4) k_rans_dec<4><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, X, err, stage_rows);
-  else if (st == 3) k_rans_dec<3><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, X, err, stage_rows);
-  else k_rans_dec<2><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, X, err, stage_rows);
+  if (st == 4) k_rans_dec<4><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, lut, X, err, stage_rows);
+  else if (st == 3) k_rans_dec<3><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, lut, X, err, stage_rows);
+  else k_rans_dec<2><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, lut, X, err, stage_rows);
   launched(c);
 }
 

@@ -874,12 +874,12 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
   for (int d = R; d < L; ++d) {
     const int8_t* Fd = net.level(d);
     const uint32_t nd = o.N[d];
-    uint16_t* cdf = buf<uint16_t>(c, "cdf", size_t(nd) * 256);
+    uint16_t* cdf = buf<uint16_t>(c, "cdf", size_t(nd) * DROW_U16);
     int8_t* a_dbg = c->debug ? buf<int8_t>(c, "t_adbg", size_t(nd) * m->H) : nullptr;
     head_any(c, Fd, nd, C, m->H, net.head_of(d), m->lut, 1, nullptr, nullptr, cdf, a_dbg);
     if (c->debug) {
       dbg_copy(c, nm("a", d), a_dbg, size_t(nd) * m->H);
-      dbg_copy(c, nm("cdf", d), cdf, size_t(nd) * 512);
+      dbg_copy(c, nm("cdf", d), cdf, size_t(nd) * DROW_BYTES);
     }
     std::vector<DecSeg> segs;
     for (int f = 0; f < B; ++f) {
@@ -894,8 +894,8 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
     DecSeg* d_segs = upload(c, "dsegs", segs);
     int kmax = 1;
     for (const DecSeg& sg : segs) kmax = std::max(kmax, lanes_for(sg.n));
-    rans_decode(c, d_segs, int(segs.size()), d_bs, cdf, static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d], err,
-                kmax);
+    rans_decode(c, d_segs, int(segs.size()), d_bs, cdf, m->lut, static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d],
+                err, kmax);
     PCC_CUDA(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s));
     PCC_CUDA(cudaStreamSynchronize(s));
     if (herr) throw Error{PCC_ERR_CORRUPT};

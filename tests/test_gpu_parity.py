@@ -195,9 +195,20 @@ def test_decoder_cdf_parity(pcc, ctx):
         for d in range(4, 12):
             p = D.get(f"p/{d}", np.uint16).reshape(-1, 255).astype(np.int64)
             cum = np.concatenate([np.zeros((p.shape[0], 1), np.int64), np.cumsum(p, 1)[:, :254]], 1)
-            got = np.frombuffer(pcc.pcc_debug_tensor(ctx, f"cdf/{d}"), np.uint16).reshape(-1, 256).astype(np.int64)
-            # row format: c[i] = C_i for i = 0..254, entry 255 unused
-            assert np.array_equal(got[:, :255], cum), d
+            raw = pcc.pcc_debug_tensor(ctx, f"cdf/{d}")
+            hdr = np.frombuffer(raw, np.uint32).reshape(-1, 148)[:, :20].astype(np.int64)
+            j = np.frombuffer(raw, np.uint16).reshape(-1, 296)[:, 40:40 + 255].astype(np.int64)
+            # decoder row: S, floor(65281 2^32 / S), E_{16k}, then the LUT
+            # index of every symbol; C_i = i + floor(E_i 65281 / S) must be the oracle's
+            lut = np.concatenate([I.exp_lut().astype(np.int64), [0]])
+            e = lut[j]
+            E = np.concatenate([np.zeros((e.shape[0], 1), np.int64), np.cumsum(e, 1)], 1)
+            S = hdr[:, 0]
+            assert np.array_equal(E[:, 255], S), d
+            assert np.array_equal(hdr[:, 1], (65281 << 32) // S), d
+            assert np.array_equal(hdr[:, 2:17], E[:, 16:241:16]), d
+            C = np.arange(255)[None, :] + (E[:, :255] * 65281) // S[:, None]
+            assert np.array_equal(C, cum), d
             assert np.array_equal(np.frombuffer(pcc.pcc_debug_tensor(ctx, f"code/{d}"), np.uint8),
                                   D.get(f"code/{d}", np.uint8)), d
     finally:
