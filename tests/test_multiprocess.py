@@ -65,3 +65,14 @@ def test_single_rank_aggregate_matches_definition():
     agg = bench.aggregate(bench.gather_stats(None, st, "cpu", 1), K=10)
     assert agg["value"] == pytest.approx(640 / 0.020)  # stats carry the summed K-step times
     assert np.isclose(agg["enc_fps"], 640 / 0.008) and np.isclose(agg["dec_fps"], 640 / 0.012)
+
+
+def test_sequence_shard_covers_every_frame_once():
+    """cfg5 (BASELINE configs[4]): the 1000-frame sequence is split by index, frame i on
+    rank i mod W, every frame on exactly one rank for W = 1..8."""
+    import bench
+    for W in range(1, 9):
+        parts = [bench.sequence_shard(r, W) for r in range(W)]
+        flat = sorted(i for p in parts for i in p)
+        assert flat == list(range(bench.SEQ_FRAMES))
+        assert max(map(len, parts)) - min(map(len, parts)) <= 1
