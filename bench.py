@@ -255,10 +255,11 @@ ALU_PEAK_NOTE = ("B200 integer issue peak = 148 SM x 4 SMSP x 32 lanes x 1 instr
 # hidden layer C*H/4 dp4a (C = H = 32) + 9 ops per symbol for the exponentials (logit
 # requant mul-add, shift, saturate; max; delta; LUT index/load/select; sum); reading Q21's
 # cumulative floors then cost the encoder one prefix add per symbol and two exact 64-bit
-# divisions per node (~10 ops each), the decoder per symbol a prefix add, scale multiply,
-# quotient, correction, index add and the store (15 per symbol in all).
+# divisions per node (~10 ops each); the decoder's predictor only stores each symbol's LUT
+# index (10 per symbol) and the 16 block prefixes: its rows carry no cumulative counts
+# (the rANS decoder rebuilds the few it searches).
 def alu_ops_per_node(C, H):
-    return {"head_enc": C * H / 4 + 10 * 255 + 20, "head_dec": C * H / 4 + 15 * 255}
+    return {"head_enc": C * H / 4 + 10 * 255 + 20, "head_dec": C * H / 4 + 10 * 255 + 16}
 
 
 def measured_traffic(kernel: str):
