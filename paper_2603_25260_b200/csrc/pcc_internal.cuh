@@ -238,7 +238,7 @@ struct DecSeg {
 // C_i = i + floor(E_i * 65281 / S) only where its search needs it.
 constexpr int DROW_BYTES = 592, DROW_HDR = 80, DROW_U16 = DROW_BYTES / 2;
 void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf,
-                 const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes);
+                 const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes, size_t nsym);
 
 // ---- pack (runtime.cu) ----
 struct PackItem {    // encoder output item: frame header+raw prefix (kind 0) or one segment (kind 1)

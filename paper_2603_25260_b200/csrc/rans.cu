@@ -215,7 +215,7 @@ void rans_encode(pcc_ctx c, const EncSeg* d_segs, int nseg, const uint32_t* cf, 
 }
 
 void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf,
-                 const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes) {
+                 const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes, size_t nsym) {
   if (nseg == 0) return;
   const int stage_rows = max_lanes <= 8 ? 8 : (max_lanes <= 16 ? 16 : 32);
   static bool attr = false;
@@ -235,7 +235,7 @@ void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, c
   }();
   if (forced >= 2 && forced <= 4) st = forced;
   const size_t smem = size_t(st) * stage_rows * DROW_BYTES;
-  Prof p(c, "rans_dec", 0);
+  Prof p(c, "rans_dec", nsym * (DROW_BYTES + 2));  // algorithmic: the row + one word per symbol
   if (st == 4) k_rans_dec<4><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, lut, X, err, stage_rows);
   else if (st == 3) k_rans_dec<3><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, lut, X, err, stage_rows);
   else k_rans_dec<2><<<nseg, 32, smem, c->stream>>>(d_segs, nseg, bs, cdf, lut, X, err, stage_rows);
