@@ -530,7 +530,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--batch", type=int, default=1024,
+                    help="frames per GPU per step (4 codec lanes of 256 frames each by default)")
     ap.add_argument("--streams", type=int, default=4, help="concurrent codec lanes (ctx + stream) per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
