@@ -62,6 +62,13 @@ def workload(args):
     return I.CONFIGS[name], C, desc
 
 
+def default_batch(name: str) -> int:
+    """Frames per GPU per step when --batch is not given: 1024 (4 lanes x 256 frames) where
+    a lane's arena fits comfortably (L <= 13), 256 for the deeper trees (L >= 14, cfg3)."""
+    deep = name == "cfg3" or (name.startswith("cfg2_L") and int(name[6:]) >= 14)
+    return 256 if deep else 1024
+
+
 def model_bytes(args, C):
     """The seeded random int8 model of --workload (n_deep = 3 for the t = L-3 variant)."""
     from paper_2603_25260_b200 import inputs as I
@@ -530,14 +537,17 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=1024,
-                    help="frames per GPU per step (4 codec lanes of 256 frames each by default)")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="frames per GPU per step (default: 1024 = 4 codec lanes x 256 frames for "
+                         "L <= 13, 256 for the deeper configs, whose per-lane arenas are larger)")
     ap.add_argument("--streams", type=int, default=4, help="concurrent codec lanes (ctx + stream) per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     args = ap.parse_args()
+    if args.batch is None:
+        args.batch = default_batch(args.workload)
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
