@@ -76,3 +76,11 @@ def test_sequence_shard_covers_every_frame_once():
         flat = sorted(i for p in parts for i in p)
         assert flat == list(range(bench.SEQ_FRAMES))
         assert max(map(len, parts)) - min(map(len, parts)) <= 1
+
+
+def test_default_batch_per_workload():
+    """bench defaults: 1024 frames per GPU (4 lanes x 256) up to L = 13, 256 for deeper trees."""
+    import bench
+    assert bench.default_batch("cfg2") == 1024 and bench.default_batch("cfg2_L13") == 1024
+    assert bench.default_batch("cfg2_L14") == 256 and bench.default_batch("cfg3") == 256
+    assert bench.default_batch("cfg2_t3") == 1024
