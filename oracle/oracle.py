@@ -15,7 +15,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "pcc_oracle.cpp")
-LIB = os.path.join(HERE, "liboracle.so")
+# PCC_ORACLE_LIB: a mutated build for tools/oracle_mutation.py only (never the product path)
+LIB = os.environ.get("PCC_ORACLE_LIB") or os.path.join(HERE, "liboracle.so")
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "EMPTY", 3: "RANGE", 4: "UNSUPPORTED_DEPTH", 5: "CAPACITY",
           6: "BAD_MAGIC", 7: "VERSION", 8: "MODEL_MISMATCH", 9: "TRUNCATED", 10: "CORRUPT",
@@ -31,6 +32,8 @@ class OracleError(RuntimeError):
 
 def build(force: bool = False) -> str:
     """Compile the oracle with plain g++ (no SIMD intrinsics, no OpenMP)."""
+    if os.environ.get("PCC_ORACLE_LIB"):
+        return LIB
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         tmp = LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["g++", "-O2", "-std=c++20", "-shared", "-fPIC", "-o", tmp, SRC])
@@ -65,6 +68,7 @@ def lib():
         L.oracle_kernel_map.argtypes = [P, S, I, P]
         L.oracle_conv3_acc.argtypes = [P, S, I, P, I, P, I, P]
         L.oracle_down_acc.argtypes = [P, S, P, S, P, I, P, P]
+        L.oracle_head_logits.argtypes = [P, S, I, I, P, P, ct.c_int32, ct.c_int32, ct.c_int32, P, P, P, P]
         L.oracle_rq.argtypes = [ct.c_int32, ct.c_int32, ct.c_int32]
         L.oracle_rq.restype = ct.c_int32
         L.oracle_prq.argtypes = [ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32]
@@ -191,6 +195,22 @@ def down_acc(child_keys, parent_keys, g, W) -> np.ndarray:
     acc = np.zeros((pk.size, C), np.int64)
     _check(lib().oracle_down_acc(_ptr(ck), ck.size, _ptr(pk), pk.size, _ptr(g), C, _ptr(W), _ptr(acc)))
     return acc
+
+
+def head_logits(F, W1, b1, rq1, W2, b2):
+    """The codec's own Eq.7 predictor: (a int8 [n, H], z int32 [n, 255])."""
+    F = np.ascontiguousarray(F, np.int8)
+    W1 = np.ascontiguousarray(W1, np.int8)
+    W2 = np.ascontiguousarray(W2, np.int8)
+    b1 = np.ascontiguousarray(b1, np.int32)
+    b2 = np.ascontiguousarray(b2, np.int32)
+    n, C = F.shape
+    H = W1.shape[0]
+    a = np.zeros((n, H), np.int8)
+    z = np.zeros((n, 255), np.int32)
+    _check(lib().oracle_head_logits(_ptr(F), n, C, H, _ptr(W1), _ptr(b1), rq1[0], rq1[1], rq1[2], _ptr(W2), _ptr(b2),
+                                    _ptr(a), _ptr(z)))
+    return a, z
 
 
 def rq(acc: int, m: int, r: int) -> int:

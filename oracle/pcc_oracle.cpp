@@ -226,14 +226,27 @@ struct Down {
 struct Deep {
   std::vector<int8_t> E;  // [255][C]
   std::vector<Down> downs;
-  std::vector<int8_t> Wa, Wb, P;  // [27][C][2C], [27][C][C], [C][2C]
+  // XFP on: Wa [27][C][2C], Wb [27][C][C], P [C][2C].  XFP off (MF_XFP_OFF): Wa, Wb
+  // [27][C][C] and the identity skip k_s (the shallow ResBlock form on G_D alone).
+  std::vector<int8_t> Wa, Wb, P;
   std::vector<int32_t> ba, bb;
+  int32_t k_s = 0;
   RQ rqa, rqb;
   std::vector<Up> ups;
   Head head;
 };
+// Model flags (model-file header word at byte 44; copied into the bitstream's flags byte):
+//   MF_XFP_OFF  the "Baseline + GRED" ablation of Table 4: deep levels
+//               drop the cross-scale concat, H = ResBlock(G_D).
+//   MF_RAW_FREQ the raw prefix X_0..X_{R-1} is coded "based on their symbol frequencies"
+//               (reading Q13', NEXT-4) instead of stored as plain bytes.
+// n_deep = 0 is the GRED-off "Baseline" of Table 4: every coded level is a
+// shallow level (Eq.8-9), directly exposed to HRCS.
+constexpr uint32_t MF_XFP_OFF = 1, MF_RAW_FREQ = 2, MF_ALL = 3;
+
 struct Model {
   int C = 0, H = 0, R = 0, n_deep = 0, min_depth = 0, max_depth = 0;
+  uint32_t flags = 0;
   uint64_t seed = 0, hash = 0;
   std::vector<uint32_t> lut;
   std::vector<int8_t> E0;
@@ -307,9 +320,23 @@ Model parse_model(const uint8_t* bytes, size_t len) {
   m.seed = r.u64();
   uint32_t lut_len = r.u32();
   if (lut_len != 1024) throw Fail{INVALID_ARG};
+  m.flags = r.u32();
+  if (m.flags & ~MF_ALL) throw Fail{INVALID_ARG};
+  // R <= 6 keeps the raw prefix (at most sum_{d<R} 8^d = 37449 nodes) inside the
+  // container's u16 raw_bytes field; n_deep in 0..4 (0 = GRED off).
+  if (m.R < 1 || m.R > 6 || m.n_deep < 0 || m.n_deep > 4 || m.C < 1 || m.H < 1 || m.C > 64 || m.H > 64 ||
+      m.min_depth < m.R + 1 + m.n_deep || m.max_depth < m.min_depth || m.max_depth > 21)
+    throw Fail{INVALID_ARG};
   r.pos = 64;
   m.lut.resize(1024);
   for (auto& x : m.lut) x = r.u32();
+  // The exp table (reading Q20) must be a valid softmax table: LUT[0] in (65281, 2^24]
+  // and non-increasing.  Then S = sum e lies in (65281, 255 * 2^24]: normalisation never
+  // divides by zero, every cumulative bound stays below 2^16 + 255, and a row's sum fits
+  // 32 bits (the width P:351 fixes for the accumulation).
+  if (m.lut[0] <= 65281u || m.lut[0] > (1u << 24)) throw Fail{INVALID_ARG};
+  for (size_t j = 1; j < m.lut.size(); ++j)
+    if (m.lut[j] > m.lut[j - 1]) throw Fail{INVALID_ARG};
   const size_t C = size_t(m.C), H = size_t(m.H);
   auto head = [&]() {
     Head h;
@@ -353,13 +380,23 @@ Model parse_model(const uint8_t* bytes, size_t len) {
       dn.rq = r.rq();
       dp.downs.push_back(std::move(dn));
     }
-    dp.Wa = r.i8v(27 * C * 2 * C);
-    dp.ba = r.i32v(C);
-    dp.rqa = r.rq();
-    dp.Wb = r.i8v(27 * C * C);
-    dp.P = r.i8v(C * 2 * C);
-    dp.bb = r.i32v(C);
-    dp.rqb = r.rq();
+    if (m.flags & MF_XFP_OFF) {  // ResBlock(G_D), same layout as a shallow ResBlock
+      dp.Wa = r.i8v(27 * C * C);
+      dp.ba = r.i32v(C);
+      dp.rqa = r.rq();
+      dp.Wb = r.i8v(27 * C * C);
+      dp.bb = r.i32v(C);
+      dp.k_s = r.i32();
+      dp.rqb = r.rq();
+    } else {
+      dp.Wa = r.i8v(27 * C * 2 * C);
+      dp.ba = r.i32v(C);
+      dp.rqa = r.rq();
+      dp.Wb = r.i8v(27 * C * C);
+      dp.P = r.i8v(C * 2 * C);
+      dp.bb = r.i32v(C);
+      dp.rqb = r.rq();
+    }
     for (int s = 0; s < j; ++s) dp.ups.push_back(up());
     dp.head = head();
     m.deep.push_back(std::move(dp));
@@ -435,19 +472,28 @@ Feat up_prune(const Up& u, const Feat& S, const std::vector<uint8_t>& X, int C) 
 
 // Eq.4 Downsampling step (reading Q4): K2S2 sparse conv, one weight matrix per
 // child index c: g_{j-1}[p] = prq(sum_{children ch of p} W_c * g_j[ch] + b).
-Feat down_step(const Down& dn, const Feat& g, const std::vector<uint64_t>& child_keys,
-               const std::vector<uint64_t>& parent_keys, int C) {
+// down_acc is the raw int64 accumulator (no bias, no requant); down_step (the codec)
+// and the test entry point oracle_down_acc both call it.  W layout [8][C_out][C_in].
+std::vector<int64_t> down_acc(const int8_t* W, const Feat& g, const std::vector<uint64_t>& child_keys,
+                              const std::vector<uint64_t>& parent_keys, int C) {
   std::vector<int64_t> acc(parent_keys.size() * C, 0);
   for (size_t ch = 0; ch < child_keys.size(); ++ch) {
     uint64_t pk = child_keys[ch] >> 3;
     size_t p = size_t(std::lower_bound(parent_keys.begin(), parent_keys.end(), pk) - parent_keys.begin());
+    if (p >= parent_keys.size() || parent_keys[p] != pk) throw Fail{INVALID_ARG};
     int c = int(child_keys[ch] & 7u);
     for (int o = 0; o < C; ++o) {
       int64_t s = 0;
-      for (int i = 0; i < C; ++i) s += int64_t(g[ch * C + i]) * int64_t(dn.W[(size_t(c) * C + o) * C + i]);
+      for (int i = 0; i < C; ++i) s += int64_t(g[ch * C + i]) * int64_t(W[(size_t(c) * C + o) * C + i]);
       acc[p * C + o] += s;
     }
   }
+  return acc;
+}
+
+Feat down_step(const Down& dn, const Feat& g, const std::vector<uint64_t>& child_keys,
+               const std::vector<uint64_t>& parent_keys, int C) {
+  std::vector<int64_t> acc = down_acc(dn.W.data(), g, child_keys, parent_keys, C);
   Feat out(parent_keys.size() * C);
   for (size_t p = 0; p < parent_keys.size(); ++p)
     for (int o = 0; o < C; ++o) out[p * C + o] = prq(to_i32(acc[p * C + o] + dn.b[o]), dn.rq.m_pos, dn.rq.m_neg, dn.rq.r);
@@ -532,8 +578,9 @@ void put_u16(std::vector<uint8_t>& o, uint32_t v) {
 
 // Encode one segment: steps in reverse, lanes K-1..0, words pushed on a stack that is
 // emitted reversed so the stream is in decoder consumption order.
-void rans_encode_segment(const uint32_t* cum, const uint32_t* freq, size_t n, std::vector<uint8_t>& out) {
-  const int K = lanes_for(n);
+void rans_encode_segment(const uint32_t* cum, const uint32_t* freq, size_t n, std::vector<uint8_t>& out,
+                         int K_force = 0) {
+  const int K = K_force > 0 ? K_force : lanes_for(n);
   std::vector<uint32_t> x(static_cast<size_t>(K), 1u << 16);
   std::vector<uint16_t> stack;
   const size_t steps = (n + size_t(K) - 1) / size_t(K);
@@ -600,6 +647,57 @@ size_t rans_decode_segment(const uint8_t* in, size_t avail, const uint32_t* p, s
   return bytes;
 }
 
+// ---- Raw prefix coder (NEXT-4; "For the geometry remaining at the maximum
+// downsampling level, we directly encode the coordinates based on their symbol
+// frequencies"; reading Q13') -------------------------------------------
+// The symbols are the raw levels' occupancy bytes X_0..X_{R-1} in level order (the
+// depth-R coordinates, losslessly).  Adaptive frequency model (SPEC S:583-584's
+// AdaptiveFreqModel): counts n_v = 1 for all 255 symbols, total T; after each symbol
+// n_v += RAW_INC, and when T exceeds RAW_LIMIT every count is halved rounding up.
+// Symbol probabilities enter the O9 rANS coder as Q16 cumulative bounds by the same
+// cumulative-floor normalisation as reading Q21: C_i = i + floor(K_i * 65281 / T),
+// K_i = sum_{u<i} n_u (C_255 = 65536, every p >= 1).  One rANS lane (K = 1): the raw
+// region is u32 W | u32 x | W u16 words | pad to 4 bytes.
+constexpr uint32_t RAW_INC = 32, RAW_LIMIT = 1u << 15;
+
+struct FreqModel {
+  uint32_t n[NCODE];
+  uint32_t T = NCODE;
+  FreqModel() {
+    for (auto& v : n) v = 1;
+  }
+  uint32_t bound(int i) const {  // C_i, i = 0..255
+    uint64_t K = 0;
+    for (int u = 0; u < i; ++u) K += n[u];
+    return uint32_t(uint64_t(i) + K * 65281u / T);
+  }
+  void update(int i) {
+    n[i] += RAW_INC;
+    T += RAW_INC;
+    if (T > RAW_LIMIT) {
+      T = 0;
+      for (auto& v : n) {
+        v = (v + 1) / 2;
+        T += v;
+      }
+    }
+  }
+};
+
+std::vector<uint8_t> raw_encode(const std::vector<uint8_t>& sym) {
+  FreqModel fm;
+  std::vector<uint32_t> cum(sym.size()), freq(sym.size());
+  for (size_t j = 0; j < sym.size(); ++j) {
+    const int i = sym[j] - 1;
+    cum[j] = fm.bound(i);
+    freq[j] = fm.bound(i + 1) - cum[j];
+    fm.update(i);
+  }
+  std::vector<uint8_t> out;
+  rans_encode_segment(cum.data(), freq.data(), sym.size(), out, 1);
+  return out;
+}
+
 // ---- Level-wise context model (Eq.2-11; readings O3, O7, Q1-Q3) -------------------
 // State carried across coded levels: the shallow chain's current feature map and F_D.
 struct Coder {
@@ -649,9 +747,32 @@ struct Coder {
       g = down_step(dp.downs[size_t(s)], g, key[kd], key[kd - 1], C);
       dump(Dp, "G/" + sd + "/" + std::to_string(kd - 1), g);
     }
+    const size_t n = key[D].size();
+    if (m.flags & MF_XFP_OFF) {
+      // "Baseline + GRED" (Table 4: "removing cross-scale feature propagation"):
+      // no Concat with F^k; H^k = ResBlock(G^k) in the Eq.8 form (reading Q7).
+      Shallow rb;
+      rb.Wa = dp.Wa; rb.ba = dp.ba; rb.rqa = dp.rqa;
+      rb.Wb = dp.Wb; rb.bb = dp.bb; rb.rqb = dp.rqb; rb.k_s = dp.k_s;
+      std::vector<int32_t> nbr = kernel_map(key[D], D);
+      Feat Hk = resblock_shallow(rb, g, nbr, n, C, nullptr, d);
+      if (Dp) {  // the same dump names as the XFP block
+        std::vector<int64_t> a = conv3_acc(nbr, n, g.data(), C, dp.Wa.data(), C);
+        Feat h(n * C);
+        for (size_t i = 0; i < n; ++i)
+          for (int o = 0; o < C; ++o) h[i * C + o] = prq(to_i32(a[i * C + o] + dp.ba[o]), dp.rqa.m_pos, dp.rqa.m_neg, dp.rqa.r);
+        dump(Dp, "hx/" + sd, h);
+        dump(Dp, "H/" + sd, Hk);
+      }
+      Feat cur = Hk;
+      for (int k = D; k < d; ++k) {
+        cur = up_prune(dp.ups[size_t(k - D)], cur, code[k], C);
+        dump(Dp, "Fp/" + sd + "/" + std::to_string(k + 1), cur);
+      }
+      return pmf_from_head(dp.head, cur, key[d].size(), d);
+    }
     // Eq.10: H^k = ResBlock(Concat(F^k, G^k)), k = t = D (reading Q2); conv_a 2C->C,
     // conv_b C->C plus a 1x1 projection of the concat as the skip (reading Q7).
-    const size_t n = key[D].size();
     Feat x(n * 2 * C);
     for (size_t i = 0; i < n; ++i)
       for (int c = 0; c < C; ++c) {
@@ -744,15 +865,18 @@ std::vector<uint8_t> encode(const Model& m, const int32_t* xyz, size_t n, int L,
   bs.push_back(uint8_t(L));
   bs.push_back(uint8_t(R));
   bs.push_back(uint8_t(m.n_deep));
-  bs.push_back(0);
-  size_t raw = 0;
-  for (int d = 0; d < R; ++d) raw += t.code[d].size();
-  put_u16(bs, uint32_t(raw));
+  bs.push_back(uint8_t(m.flags));
+  std::vector<uint8_t> rawsym;
+  for (int d = 0; d < R; ++d) rawsym.insert(rawsym.end(), t.code[d].begin(), t.code[d].end());
+  // reading Q13: plain bytes; MF_RAW_FREQ: the adaptive symbol-frequency coder
+  std::vector<uint8_t> rawreg = (m.flags & MF_RAW_FREQ) ? raw_encode(rawsym) : rawsym;
+  if (rawreg.size() > 0xFFFFu) throw Fail{CAPACITY};
+  put_u16(bs, uint32_t(rawreg.size()));
   put_u32(bs, uint32_t(t.key[L].size()));
   put_u32(bs, uint32_t(m.hash));
   put_u32(bs, uint32_t(m.hash >> 32));
   for (auto& pl : payload) put_u32(bs, uint32_t(pl.size()));
-  for (int d = 0; d < R; ++d) bs.insert(bs.end(), t.code[d].begin(), t.code[d].end());  // reading Q13
+  bs.insert(bs.end(), rawreg.begin(), rawreg.end());
   while (bs.size() % 4) bs.push_back(0);
   for (auto& pl : payload) bs.insert(bs.end(), pl.begin(), pl.end());
   return bs;
@@ -766,7 +890,7 @@ std::vector<uint64_t> decode(const Model& m, const uint8_t* bs, size_t len, int&
   const size_t raw = uint32_t(bs[10]) | uint32_t(bs[11]) << 8;
   const uint32_t NL = get_u32(bs + 12);
   const uint64_t hash = uint64_t(get_u32(bs + 16)) | uint64_t(get_u32(bs + 20)) << 32;
-  if (hash != m.hash || R != m.R || nd != m.n_deep) throw Fail{MODEL_MISMATCH};
+  if (hash != m.hash || R != m.R || nd != m.n_deep || bs[9] != m.flags) throw Fail{MODEL_MISMATCH};
   check_depth(m, L);
   L_out = L;
   size_t pos = 24;
@@ -777,17 +901,50 @@ std::vector<uint64_t> decode(const Model& m, const uint8_t* bs, size_t len, int&
   std::vector<std::vector<uint64_t>> key(static_cast<size_t>(L + 1));
   std::vector<std::vector<uint8_t>> code(static_cast<size_t>(L));
   key[0] = {0};
-  size_t rp = 0;
-  for (int d = 0; d < R; ++d) {  // raw prefix (reading O4/Q13)
-    const size_t N = key[d].size();
-    if (rp + N > raw || pos + rp + N > len) throw Fail{raw < rp + N ? CORRUPT : TRUNCATED};
-    code[d].assign(bs + pos + rp, bs + pos + rp + N);
-    for (uint8_t c : code[d])
-      if (c == 0) throw Fail{CORRUPT};
-    rp += N;
-    key[d + 1] = expand(key[d], code[d]);
+  if (pos + raw > len) throw Fail{TRUNCATED};
+  if (m.flags & MF_RAW_FREQ) {  // adaptive symbol-frequency raw prefix, one rANS lane
+    const uint8_t* p = bs + pos;
+    if (raw < 8) throw Fail{CORRUPT};
+    const uint32_t W = get_u32(p);
+    uint32_t x = get_u32(p + 4);
+    if (raw != 8 + 4 * ((size_t(W) + 1) / 2) || x < (1u << 16)) throw Fail{CORRUPT};
+    const uint8_t* w = p + 8;
+    size_t wp = 0;
+    FreqModel fm;
+    for (int d = 0; d < R; ++d) {
+      const size_t N = key[d].size();
+      code[d].assign(N, 0);
+      for (size_t k = 0; k < N; ++k) {
+        const uint32_t slot = x & 0xFFFFu;
+        int i = 0;
+        while (fm.bound(i + 1) <= slot) ++i;  // CDF^-1(slot)
+        const uint32_t c = fm.bound(i), f = fm.bound(i + 1) - c;
+        x = f * (x >> 16) + slot - c;
+        if (x < (1u << 16)) {
+          if (wp >= W) throw Fail{CORRUPT};
+          x = (x << 16) | (uint32_t(w[2 * wp]) | uint32_t(w[2 * wp + 1]) << 8);
+          ++wp;
+        }
+        code[d][k] = uint8_t(i + 1);
+        fm.update(i);
+      }
+      key[d + 1] = expand(key[d], code[d]);
+      if (key[d + 1].size() > NL) throw Fail{CORRUPT};
+    }
+    if (wp != W || x != (1u << 16)) throw Fail{CORRUPT};
+  } else {
+    size_t rp = 0;
+    for (int d = 0; d < R; ++d) {  // raw prefix (reading O4/Q13)
+      const size_t N = key[d].size();
+      if (rp + N > raw) throw Fail{CORRUPT};
+      code[d].assign(bs + pos + rp, bs + pos + rp + N);
+      for (uint8_t c : code[d])
+        if (c == 0) throw Fail{CORRUPT};
+      rp += N;
+      key[d + 1] = expand(key[d], code[d]);
+    }
+    if (rp != raw) throw Fail{CORRUPT};
   }
-  if (rp != raw) throw Fail{CORRUPT};
   pos += (raw + 3) / 4 * 4;
   Coder cd(m, L, Dp);
   for (int d = R; d < L; ++d) {
@@ -913,20 +1070,33 @@ int oracle_conv3_acc(const uint64_t* keys, size_t n, int depth, const int8_t* f,
   })
 }
 
-// K2S2 down step with identity requant exposed as raw accumulators: parents given.
+// Raw accumulators of the codec's own K2S2 down step (down_acc, called by down_step).
 int oracle_down_acc(const uint64_t* child_keys, size_t nc, const uint64_t* parent_keys, size_t np,
                     const int8_t* g, int C, const int8_t* W, int64_t* acc) {
   ORACLE_TRY({
     std::vector<uint64_t> ck(child_keys, child_keys + nc), pk(parent_keys, parent_keys + np);
-    std::vector<int64_t> a(np * size_t(C), 0);
-    for (size_t ch = 0; ch < nc; ++ch) {
-      size_t p = size_t(std::lower_bound(pk.begin(), pk.end(), ck[ch] >> 3) - pk.begin());
-      if (p >= np || pk[p] != (ck[ch] >> 3)) throw Fail{INVALID_ARG};
-      int c = int(ck[ch] & 7u);
-      for (int o = 0; o < C; ++o)
-        for (int i = 0; i < C; ++i) a[p * C + o] += int64_t(g[ch * C + i]) * int64_t(W[(size_t(c) * C + o) * C + i]);
-    }
+    Feat gv(g, g + nc * size_t(C));
+    std::vector<int64_t> a = down_acc(W, gv, ck, pk, C);
     std::memcpy(acc, a.data(), a.size() * sizeof(int64_t));
+  })
+}
+
+// The codec's own Eq.7 predictor (head_logits) on explicit weights: a [n][H] int8 and
+// z [n][255] int32.
+int oracle_head_logits(const int8_t* F, size_t n, int C, int H, const int8_t* W1, const int32_t* b1, int32_t mp,
+                       int32_t mn, int32_t r, const int8_t* W2, const int32_t* b2, int8_t* a_out, int32_t* z_out) {
+  ORACLE_TRY({
+    Head h;
+    h.W1.assign(W1, W1 + size_t(H) * C);
+    h.b1.assign(b1, b1 + H);
+    h.rq1 = RQ{mp, mn, r};
+    h.W2.assign(W2, W2 + size_t(NCODE) * H);
+    h.b2.assign(b2, b2 + NCODE);
+    Feat f(F, F + n * size_t(C));
+    Dump D;
+    std::vector<int32_t> z = head_logits(h, f, n, C, H, &D, 0);
+    std::memcpy(a_out, D.t["a/0"].data(), n * size_t(H));
+    std::memcpy(z_out, z.data(), z.size() * sizeof(int32_t));
   })
 }
 

@@ -165,6 +165,10 @@ def random_cloud(n: int, bit_depth: int, seed: int, spread: float = 1.0) -> np.n
 # ---------------------------------------------------------------------------
 
 MODEL_MAGIC = b"PCCM"
+# model-file flags (header word at byte 44): the Table 4 ablation without
+# cross-scale propagation and the symbol-frequency raw-prefix coder
+FLAG_XFP_OFF = 1
+FLAG_RAW_FREQ = 2
 MODEL_VERSION = 1
 LUT_LEN = 1024
 N_CODES = 255
@@ -227,10 +231,11 @@ class Down:
 class Deep:
     E: np.ndarray                          # int8 [255, C]
     downs: List[Down]                      # j-1 steps, depth d-1 -> D
-    Wa: np.ndarray; ba: np.ndarray; rqa: RQ                  # conv3 2C->C
-    Wb: np.ndarray; P: np.ndarray; bb: np.ndarray; rqb: RQ   # conv3 C->C + 1x1 2C->C
+    Wa: np.ndarray; ba: np.ndarray; rqa: RQ                  # conv3 2C->C (C->C with XFP off)
+    Wb: np.ndarray; P: np.ndarray; bb: np.ndarray; rqb: RQ   # conv3 C->C + 1x1 2C->C (P None: XFP off)
     ups: List[Up]                          # j steps, depth D -> d
     head: Head
+    k_s: int = 0                           # XFP off: identity skip k_s * G_D
 
 
 @dataclasses.dataclass
@@ -246,6 +251,7 @@ class Model:
     E0: np.ndarray                      # int8 [255, C]
     shallow: Dict[int, Shallow]         # absolute depth d in [R, max_depth - 1 - n_deep]
     deep: List[Deep]                    # j = 1..n_deep (index j-1)
+    flags: int = 0                      # FLAG_XFP_OFF | FLAG_RAW_FREQ
 
     # -- serialisation (DESIGN.md §"Model file") --------------------------
     def to_bytes(self) -> bytes:
@@ -253,7 +259,7 @@ class Model:
         out += MODEL_MAGIC
         out += struct.pack("<7I", MODEL_VERSION, self.C, self.H, self.R, self.n_deep,
                            self.min_depth, self.max_depth)
-        out += struct.pack("<QII", self.seed, LUT_LEN, 0)
+        out += struct.pack("<QII", self.seed, LUT_LEN, self.flags)
         out += bytes(64 - len(out))
         assert len(out) == 64
         out += self.lut.astype("<u4").tobytes()
@@ -295,8 +301,12 @@ class Model:
             assert len(dp.downs) == j - 1 and len(dp.ups) == j
             for dn in dp.downs:
                 out += i8(dn.W, (8, C, C)) + i32(dn.b, (C,)) + rq(dn.rq)
-            out += i8(dp.Wa, (27, C, 2 * C)) + i32(dp.ba, (C,)) + rq(dp.rqa)
-            out += i8(dp.Wb, (27, C, C)) + i8(dp.P, (C, 2 * C)) + i32(dp.bb, (C,)) + rq(dp.rqb)
+            if self.flags & FLAG_XFP_OFF:   # ResBlock(G_D): the shallow ResBlock layout
+                out += i8(dp.Wa, (27, C, C)) + i32(dp.ba, (C,)) + rq(dp.rqa)
+                out += i8(dp.Wb, (27, C, C)) + i32(dp.bb, (C,)) + struct.pack("<i", dp.k_s) + rq(dp.rqb)
+            else:
+                out += i8(dp.Wa, (27, C, 2 * C)) + i32(dp.ba, (C,)) + rq(dp.rqa)
+                out += i8(dp.Wb, (27, C, C)) + i8(dp.P, (C, 2 * C)) + i32(dp.bb, (C,)) + rq(dp.rqb)
             for u in dp.ups:
                 out += up(u)
             out += head(dp.head)
@@ -330,17 +340,22 @@ def _rq_for(acc_std: float, prelu: bool, target_std: float = NOMINAL_ACT_STD, r:
 
 
 def make_model(C: int = 32, H: int = 32, seed: int = 1, R: int = 4, n_deep: int = 4,
-               min_depth: int = 9, max_depth: int = 18, kind: str = "random") -> Model:
+               min_depth: int = 9, max_depth: int = 18, kind: str = "random", xfp: bool = True,
+               raw_freq: bool = False) -> Model:
     """Seeded random integer model (DESIGN.md §"Model generator").
 
     kind = "random" | "zero" (all weights/biases/tables 0) | "bias_head"
     (random network, W2 = 0 so every node's logits are b2).
+    Table 4 ablations: xfp=False is "Baseline + GRED" (deep levels code
+    from H = ResBlock(G_D) alone); n_deep=0 is the GRED-off "Baseline" (every level a
+    shallow level).  raw_freq=True codes the raw prefix with the adaptive
+    symbol-frequency coder instead of plain bytes.
     Magnitudes follow a nominal activation std of 40 with requant multipliers
     set from each layer's nominal fan-in, so activations neither saturate nor
     collapse (SURVEY §7 hard part (f)).
     """
     assert C % 8 == 0 and H % 8 == 0 and 8 <= C <= 64 and 8 <= H <= 64
-    assert R + 1 + n_deep <= min_depth <= max_depth <= 21
+    assert R + 1 + n_deep <= min_depth <= max_depth <= 21 and 0 <= n_deep <= 4 and 1 <= R <= 6
     rng = np.random.default_rng(seed)
     sa = NOMINAL_ACT_STD
     sw = W_MAX / np.sqrt(3.0)
@@ -394,13 +409,21 @@ def make_model(C: int = 32, H: int = 32, seed: int = 1, R: int = 4, n_deep: int 
         for _ in range(j - 1):
             s = sa * sw * np.sqrt(3 * C)
             downs.append(Down(w(8, C, C), bias(C, s), _rq_for(s, True)))
+        if not xfp:   # ResBlock(G_D) in the shallow form (C -> C, identity skip k_s)
+            sc = sa * sw * np.sqrt(7 * C)
+            k_s = 0 if zero else int(round(sc / sa))
+            deep.append(Deep(E, downs, w(27, C, C), bias(C, sc), _rq_for(sc, True),
+                             w(27, C, C), None, bias(C, sc), _rq_for(np.sqrt(2) * sc, False),
+                             [up() for _ in range(j)], head(), k_s))
+            continue
         sa2 = sa * sw * np.sqrt(7 * 2 * C)
         sb = sa * sw * np.sqrt(7 * C)
         sp = sa * sw * np.sqrt(2 * C)
         deep.append(Deep(E, downs, w(27, C, 2 * C), bias(C, sa2), _rq_for(sa2, True),
                          w(27, C, C), w(C, 2 * C), bias(C, sb), _rq_for(np.hypot(sb, sp), False),
                          [up() for _ in range(j)], head()))
-    return Model(C, H, R, n_deep, min_depth, max_depth, seed, exp_lut(), E0, shallow, deep)
+    flags = (0 if xfp else FLAG_XFP_OFF) | (FLAG_RAW_FREQ if raw_freq else 0)
+    return Model(C, H, R, n_deep, min_depth, max_depth, seed, exp_lut(), E0, shallow, deep, flags)
 
 
 def model_bytes(C: int = 32, H: int = 32, seed: int = 1, **kw) -> bytes:
