@@ -59,10 +59,44 @@ typedef struct pcc_model_s* pcc_model;
  * thread-safe.  Reuse one ctx across calls to avoid steady-state allocation. */
 typedef struct pcc_ctx_s* pcc_ctx;
 
+/* Model flags (model-file header word at byte 44, stamped into every bitstream):
+ *  PCC_MODEL_XFP_OFF  Table 4's "Baseline + GRED" ablation: deep levels
+ *                     code from H = ResBlock(G_D) without the cross-scale concat of Eq.10.
+ *  PCC_MODEL_RAW_FREQ the raw prefix X_0..X_{R-1} is coded "based on their symbol
+ *                     frequencies" (adaptive counts + one rANS lane, DESIGN.md
+ *                     reading Q13') instead of stored as plain bytes (reading Q13).
+ * deep_levels = 0 is Table 4's GRED-off "Baseline": every level shallow. */
+#define PCC_MODEL_XFP_OFF 1u
+#define PCC_MODEL_RAW_FREQ 2u
+
+/* Architecture of a model.  channels C in {8, 16, 32}; head_hidden H = C
+ * (reading Q9); raw_levels R in [1, 6] (reading Q12); deep_levels n_deep in [0, 4] (4 = the
+ * paper's t = L - 4; 3 = the t = L - 3 ablation; 0 = GRED off); the model
+ * codes bit depths L in [min_depth, max_depth] with R + 1 + n_deep <= min_depth and
+ * max_depth <= 21 (63-bit Morton keys); seed of the random initialisation; flags above. */
+typedef struct {
+  int channels, head_hidden, raw_levels, deep_levels, min_depth, max_depth;
+  uint64_t seed;
+  uint32_t flags;
+} pcc_model_config;
+
 /* Model file = DESIGN.md §4 "Model file" (little-endian, FNV-1a-64 trailer).
- * Parses, validates the hash, uploads to the current device. */
+ * Parses and validates it (hash -> MODEL_MISMATCH; layout, exp table outside
+ * (65281, 2^24] or increasing, unsupported shape -> INVALID_ARG) and uploads it to
+ * `device`.  The caller keeps ownership of `bytes`. */
 pcc_status pcc_model_load(const void* bytes, size_t len, int device, pcc_model* out);
+/* Seeded random-init integer model of the architecture `cfg` (int8 weights, int32
+ * biases, fixed-point requant triples and the exp LUT; no trained checkpoint
+ * exists offline), uploaded to `device`.  INVALID_ARG for an unsupported cfg. */
+pcc_status pcc_model_create_random(const pcc_model_config* cfg, int device, pcc_model* out);
+/* The same model FILE as pcc_model_create_random builds, written to host memory without
+ * touching a GPU (buf may be NULL to query *len).  CAPACITY if cap < *len. */
+pcc_status pcc_model_random_file(const pcc_model_config* cfg, void* buf, size_t cap, size_t* len);
+/* Serialise a loaded / created model to its model file (host buf, cap bytes).  *len =
+ * file size; CAPACITY (with *len set) if cap is too small; buf may be NULL to query. */
+pcc_status pcc_model_save(pcc_model m, void* buf, size_t cap, size_t* len);
 pcc_status pcc_model_hash(pcc_model m, uint64_t* out);
+pcc_status pcc_model_flags(pcc_model m, uint32_t* out);
 /* channels C, head hidden H, raw levels R, deep levels n_deep, min/max depth. */
 pcc_status pcc_model_info(pcc_model m, int* C, int* H, int* R, int* n_deep, int* min_depth, int* max_depth);
 void pcc_model_destroy(pcc_model m);
@@ -94,17 +128,29 @@ pcc_status pcc_build_octree(pcc_ctx c, const int32_t* d_xyz, size_t n, int bit_d
 pcc_status pcc_hrcs_stats(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int frames, int bit_depth,
                           uint64_t* h_nodes, uint64_t* h_nbr);
 
-/* Encode one frame: d_xyz device int32 [n][3] -> bitstream at d_out (device,
- * out_cap bytes).  *out_len = bytes written (or required, on CAPACITY). */
+/* Encode one frame (the paper's encoder, Fig.2 / P:139-151): octree of the Morton-sorted
+ * unique voxels, level-wise occupancy prediction "in a layer-wise
+ * autoregressive manner" (Eq.2) by the integer-only GRED/XFP network (Eq.4-14),
+ * the Eq.15 integer softmax, and entropy coding of the occupancy symbols with the
+ * predicted distributions.  d_xyz device int32 [n][3] -> bitstream at d_out
+ * (device, out_cap bytes).  *out_len = bytes written (or required, on CAPACITY).  Errors:
+ * EMPTY (n = 0), RANGE, UNSUPPORTED_DEPTH, CAPACITY, CUDA, OOM. */
 pcc_status pcc_encode(pcc_ctx c, pcc_model m, const int32_t* d_xyz, size_t n, int bit_depth,
                       uint8_t* d_out, size_t out_cap, size_t* out_len);
 
-/* Decode one bitstream (device bytes d_bs[len]) into d_xyz_out (device int32
- * [cap_points][3]).  *n_out = unique voxels, *bit_depth_out = L from the header. */
+/* Decode one bitstream (Eq.2: level l's distribution depends only on decoded levels < l,
+ * P:177-184, so decoding is level-serial and parallel within a level; the decoder
+ * expands each decoded level as P:654-655 describes).  d_bs: device bytes d_bs[len];
+ * output d_xyz_out device int32 [cap_points][3]: the unique voxels in Morton order.
+ * *n_out = unique voxels, *bit_depth_out = L from the header.  Validation order: magic
+ * (BAD_MAGIC), version (VERSION), model hash / R / n_deep / flags (MODEL_MISMATCH)
+ * before any entropy decoding; TRUNCATED / CORRUPT never hang; CAPACITY sets *n_out. */
 pcc_status pcc_decode(pcc_ctx c, pcc_model m, const uint8_t* d_bs, size_t len,
                       int32_t* d_xyz_out, size_t cap_points, size_t* n_out, int* bit_depth_out);
 
-/* Throughput variants: `frames` frames concatenated.  offs / bs_offs are HOST
+/* Throughput variants (the frame-level data parallelism of BASELINE.json north_star;
+ * frames are independent, P:651-660 builds each frame's octree on its own): `frames`
+ * frames concatenated.  offs / bs_offs are HOST
  * arrays of frames+1 prefix offsets (points / bytes).  All frames of a batch
  * share bit_depth.  out_offs (HOST, frames+1) receives the per-frame bitstream
  * (encode, bytes) or voxel (decode, points) prefix offsets into d_out /

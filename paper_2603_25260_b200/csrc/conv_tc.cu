@@ -289,11 +289,7 @@ void launch(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const i
             const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out) {
   constexpr int smem = 27 * SLABS * 1024 + (SKIP == 2 ? 2048 : 0) + 2 * group_of(SLABS) * SLABS * 4096 + 64 + 128;
   auto kern = k_conv3_tc<SLABS, SKIP>;
-  static bool attr = false;
-  if (!attr) {
-    PCC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  PCC_SMEM_ATTR(kern, smem);
   // the zero row n belongs to tile n / CT: cover rows 0..n
   const uint32_t ntiles = (n + 1 + CT - 1) / CT;
   const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 3u));

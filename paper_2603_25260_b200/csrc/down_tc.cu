@@ -146,12 +146,8 @@ __global__ void __launch_bounds__(DNT, 1) k_down_tc(const int8_t* __restrict__ g
 void down_tc(pcc_ctx c, const int8_t* g, const uint8_t* Xp, const uint32_t* cs_p, uint32_t np, const DDown& L,
              int8_t* out) {
   constexpr int smem = SM_END;  // ~136 KB: one CTA (four tile groups) per SM
-  static bool attr = false;
-  if (!attr) {
-    PCC_CUDA(cudaFuncSetAttribute(k_down_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    PCC_CUDA(cudaFuncSetAttribute(k_down_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  PCC_SMEM_ATTR(k_down_tc<true>, smem);
+  PCC_SMEM_ATTR(k_down_tc<false>, smem);
   const uint32_t ntiles = (np + 127) / 128;
   const unsigned grid = std::max(1u, std::min((ntiles + DG - 1) / DG, unsigned(c->sm_count)));
   Prof p(c, "down", size_t(np) * (1 + 4 + 32));

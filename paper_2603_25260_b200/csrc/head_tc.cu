@@ -477,11 +477,7 @@ template <int C, int H, int MODE, bool SAT>
 void launch_head(pcc_ctx c, const int8_t* F, uint32_t n, const DHead& L, const uint32_t* lut, const uint8_t* X,
                  uint32_t* cf, uint16_t* cdf, int8_t* a_dbg) {
   auto kern = k_head_tc<C, H, MODE, SAT>;
-  static bool attr = false;
-  if (!attr) {
-    PCC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemLayout<MODE>::END));
-    attr = true;
-  }
+  PCC_SMEM_ATTR(kern, SmemLayout<MODE>::END);
   const uint32_t ntiles = (n + TILE - 1) / TILE;
   const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 2u));
   kern<<<grid, NT, SmemLayout<MODE>::END, c->stream>>>(F, n, L.W1, L.b1, L.rq1, L.W2, L.b2, L.rql, lut, X, cf, cdf, a_dbg,
@@ -512,11 +508,7 @@ void head_cdf_tc(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHe
 
 void gemm_i8_test(pcc_ctx c, const int8_t* dA, const int8_t* dB, int N, int32_t* dD) {
   if (N < 32 || N > 256 || N % 32) throw Error{PCC_ERR_INVALID_ARG};
-  static bool attr = false;
-  if (!attr) {
-    PCC_CUDA(cudaFuncSetAttribute(k_gemm_i8_test, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
-    attr = true;
-  }
+  PCC_SMEM_ATTR(k_gemm_i8_test, 80 * 1024);
   k_gemm_i8_test<<<1, 128, 80 * 1024, c->stream>>>(dA, dB, N, dD);
   launched(c);
 }

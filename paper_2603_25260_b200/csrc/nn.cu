@@ -345,11 +345,7 @@ void launch_conv3(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, c
                   const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out) {
   const size_t smem = (27 * COUT * (CIN / 4) + (SKIP == 2 ? COUT * (2 * COUT / 4) : 0)) * sizeof(int32_t);
   auto kern = k_conv3<CIN, COUT, C0, SKIP>;
-  static bool attr = false;
-  if (!attr) {
-    PCC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  PCC_SMEM_ATTR(kern, 200 * 1024);
   Prof p(c, "conv", size_t(n) * (CIN + COUT + 27 * 4 + (SKIP ? (SKIP == 2 ? 2 * COUT : COUT) : 0)));
   kern<<<cdiv(size_t(n) + 1, 128), 128, smem, c->stream>>>(in0, in1, n, nbr, L.W, L.b, L.rq, s0, s1, k_s, P, out);
   launched(c);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <map>
 #include <string>
 #include <vector>
@@ -74,18 +75,27 @@ struct DDown {       // K2S2: W [8][C][C], b [C]
 struct DDeep {
   const int8_t* E;   // [255][C]
   DDown down[3];
-  DConv a;           // [27][C][2C]
+  DConv a;           // [27][C][2C]  (XFP off: [27][C][C])
   DConv b;           // [27][C][C]
-  const int8_t* P;   // [C][2C]
+  const int8_t* P;   // [C][2C]      (XFP off: null, identity skip k_s * G_D instead)
+  int32_t k_s;
   DUp up[4];
   DHead head;
 };
 
 }  // namespace pcc
 
+// Model flags (DESIGN.md §4 "Model file", header word at byte 44; stamped into the
+// bitstream's flags byte): the Table 4 "Baseline + GRED" ablation without cross-scale
+// propagation and the P:601 symbol-frequency raw-prefix coder.  n_deep = 0 is the
+// GRED-off "Baseline".
+enum : uint32_t { MF_XFP_OFF = 1u, MF_RAW_FREQ = 2u, MF_ALL = 3u };
+
 struct pcc_model_s {
   int device = 0;
   int C = 0, H = 0, R = 0, n_deep = 0, min_depth = 0, max_depth = 0;
+  uint32_t flags = 0;
+  std::vector<uint8_t> file;  // the model file image (pcc_model_save)
   uint64_t hash = 0;
   void* dmem = nullptr;
   const uint32_t* lut = nullptr;
@@ -134,6 +144,21 @@ struct Error {
   do {                                                   \
     cudaError_t e_ = (x);                                \
     if (e_ != cudaSuccess) throw ::pcc::Error{e_ == cudaErrorMemoryAllocation ? PCC_ERR_OOM : PCC_ERR_CUDA}; \
+  } while (0)
+
+// One-time, per-device, thread-safe cudaFuncSetAttribute(MaxDynamicSharedMemorySize) at
+// a launch site: the attribute is set on the current device before its bit is published,
+// so a thread that sees the bit also sees the attribute; a race only sets it twice.
+#define PCC_SMEM_ATTR(kern, bytes)                                                           \
+  do {                                                                                       \
+    static std::atomic<uint64_t> attr_mask_{0};                                              \
+    int dev_ = 0;                                                                            \
+    PCC_CUDA(cudaGetDevice(&dev_));                                                          \
+    const uint64_t bit_ = 1ull << (dev_ & 63);                                               \
+    if (!(attr_mask_.load(std::memory_order_acquire) & bit_)) {                              \
+      PCC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes))); \
+      attr_mask_.fetch_or(bit_, std::memory_order_release);                                  \
+    }                                                                                        \
   } while (0)
 
 // Workspace arena: named buffers, grown on demand, never shrunk.
@@ -239,6 +264,20 @@ struct DecSeg {
 constexpr int DROW_BYTES = 592, DROW_HDR = 80, DROW_U16 = DROW_BYTES / 2;
 void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf,
                  const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes, size_t nsym);
+
+// ---- modelgen.cu ----
+bool model_config_valid(const pcc_model_config& c);
+std::vector<uint8_t> random_model_file(const pcc_model_config& c);
+
+// ---- rawcoder.cu (raw prefix X_0..X_{R-1}: plain bytes, or the P:601 frequency coder) ----
+uint32_t raw_max_symbols(int R);  // sum_{d<R} 8^d
+// sz[f] = raw region bytes of frame f; freq: region written at region + f * cap
+void raw_encode(pcc_ctx c, bool freq, const uint8_t* code, const uint64_t* d_nb, const uint32_t* d_foff, int B, int R,
+                uint8_t* region, uint32_t cap, uint32_t* sz);
+// decodes the frequency-coded regions: symbols at sym + f * raw_max_symbols(R), node
+// counts per depth cnt[f * (R + 1) + d] (0 at d = R and EF_CORRUPT on a bad region)
+void raw_decode(pcc_ctx c, const uint8_t* bs, const uint64_t* raw_off, const uint32_t* raw_len, int B, int R,
+                const uint32_t* d_NL, uint8_t* sym, uint32_t* cnt, uint32_t* err);
 
 // ---- pack (runtime.cu) ----
 struct PackItem {    // encoder output item: frame header+raw prefix (kind 0) or one segment (kind 1)

@@ -218,13 +218,9 @@ void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, c
                  const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes, size_t nsym) {
   if (nseg == 0) return;
   const int stage_rows = max_lanes <= 8 ? 8 : (max_lanes <= 16 ? 16 : 32);
-  static bool attr = false;
-  if (!attr) {
-    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 32 * DROW_BYTES));
-    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32 * DROW_BYTES));
-    PCC_CUDA(cudaFuncSetAttribute(k_rans_dec<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * DROW_BYTES));
-    attr = true;
-  }
+  PCC_SMEM_ATTR(k_rans_dec<2>, 2 * 32 * DROW_BYTES);
+  PCC_SMEM_ATTR(k_rans_dec<3>, 3 * 32 * DROW_BYTES);
+  PCC_SMEM_ATTR(k_rans_dec<4>, 4 * 32 * DROW_BYTES);
   // two stages: measured best on the B = 256 bench (2.55 ms vs 2.87 / 3.02 ms per step for
   // 3 / 4 stages): the decode is bandwidth-bound on the largest levels, where more CTAs
   // resident per SM beat deeper prefetch

@@ -231,13 +231,28 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
     m->min_depth = int(r.u32());
     m->max_depth = int(r.u32());
     const int C = m->C, H = m->H;
-    if (!(C == 8 || C == 16 || C == 32) || H != C || m->n_deep < 1 || m->n_deep > 4 || m->R < 1 || m->max_depth > MAX_DEPTH ||
-        m->min_depth < m->R + 1 + m->n_deep || m->max_depth < m->min_depth)
+    // n_deep = 0: the GRED-off Table 4 "Baseline" (every level shallow); R <= 6 keeps the
+    // raw prefix (<= 37449 nodes) inside the container's u16 raw_bytes field
+    if (!(C == 8 || C == 16 || C == 32) || H != C || m->n_deep < 0 || m->n_deep > 4 || m->R < 1 || m->R > 6 ||
+        m->max_depth > MAX_DEPTH || m->min_depth < m->R + 1 + m->n_deep || m->max_depth < m->min_depth)
       throw Error{PCC_ERR_INVALID_ARG};
     r.pos = 40;
     if (r.u32() != 1024) throw Error{PCC_ERR_INVALID_ARG};
+    m->flags = r.u32();
+    if (m->flags & ~MF_ALL) throw Error{PCC_ERR_INVALID_ARG};
     r.pos = 64;
     Stage st;
+    {
+      // exp table (reading Q20) must be a softmax table: LUT[0] in (65281, 2^24] and
+      // non-increasing, so S = sum e lies in (65281, 255 * 2^24]: u32 row sums, no division
+      // by zero, and inv32 = floor(65281 * 2^32 / S) < 2^32 (the decoder rows)
+      if (len < 64 + 4096 + 8) throw Error{PCC_ERR_INVALID_ARG};
+      uint32_t lut[1024];
+      std::memcpy(lut, bytes + 64, 4096);
+      if (lut[0] <= 65281u || lut[0] > (1u << 24)) throw Error{PCC_ERR_INVALID_ARG};
+      for (int j = 1; j < 1024; ++j)
+        if (lut[j] > lut[j - 1]) throw Error{PCC_ERR_INVALID_ARG};
+    }
     size_t o_lut = st.put(r.take(4096), 4096);
     size_t o_E0 = st.put(r.take(size_t(NCODE) * C), size_t(NCODE) * C);
     auto conv = [&](int cin) {
@@ -314,17 +329,28 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
         dp.down[s].b = off_ptr<const int32_t>(st.put(r.take(size_t(4) * C), size_t(4) * C));
         dp.down[s].rq = r.rq();
       }
-      dp.a = conv(2 * C);
-      dp.a.rq = r.rq();
-      dp.b.W = off_ptr<const int8_t>(st.put(r.take(size_t(27) * C * C), size_t(27) * C * C));
-      dp.P = off_ptr<const int8_t>(st.put(r.take(size_t(C) * 2 * C), size_t(C) * 2 * C));
-      dp.b.b = off_ptr<const int32_t>(st.put(r.take(size_t(4) * C), size_t(4) * C));
-      dp.b.rq = r.rq();
+      if (m->flags & MF_XFP_OFF) {  // ResBlock(G_D) in the shallow layout (P:528 ablation)
+        dp.a = conv(C);
+        dp.a.rq = r.rq();
+        dp.b = conv(C);
+        dp.k_s = r.i32();
+        dp.b.rq = r.rq();
+        dp.P = nullptr;
+      } else {
+        dp.a = conv(2 * C);
+        dp.a.rq = r.rq();
+        dp.b.W = off_ptr<const int8_t>(st.put(r.take(size_t(27) * C * C), size_t(27) * C * C));
+        dp.P = off_ptr<const int8_t>(st.put(r.take(size_t(C) * 2 * C), size_t(C) * 2 * C));
+        dp.b.b = off_ptr<const int32_t>(st.put(r.take(size_t(4) * C), size_t(4) * C));
+        dp.b.rq = r.rq();
+        dp.k_s = 0;
+      }
       for (int s = 0; s < j; ++s) dp.up[s] = up();
       dp.head = head();
       m->deep.push_back(dp);
     }
     if (r.pos != r.n) throw Error{PCC_ERR_INVALID_ARG};
+    m->file.assign(bytes, bytes + len);
     PCC_CUDA(cudaSetDevice(device));
     PCC_CUDA(cudaMalloc(&m->dmem, st.img.size()));
     PCC_CUDA(cudaMemcpy(m->dmem, st.img.data(), st.img.size(), cudaMemcpyHostToDevice));
@@ -349,7 +375,7 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
       for (int s = 0; s < j - 1; ++s) { dp.down[s].W = rebase(dp.down[s].W, base); dp.down[s].b = rebase(dp.down[s].b, base); }
       dp.a.W = rebase(dp.a.W, base); dp.a.b = rebase(dp.a.b, base);
       dp.b.W = rebase(dp.b.W, base); dp.b.b = rebase(dp.b.b, base);
-      dp.P = rebase(dp.P, base);
+      if (dp.P) dp.P = rebase(dp.P, base);
       for (int s = 0; s < j; ++s) rb_up(dp.up[s]);
       rb_head(dp.head);
     }
@@ -463,13 +489,20 @@ struct Net {
       std::swap(ga, gb);
       dbgF(nm("G", d, k - 1), ga, o.N[k - 1], C);
     }
-    // Eq.10: H = ResBlock(Concat(F_D, G_D)), virtual concat, 1x1 projection skip
     const uint32_t nD = o.N[D];
     int8_t* hx = buf<int8_t>(c, "t_hx", rows(D) * C);
     int8_t* Hk = buf<int8_t>(c, "t_H", rows(D) * C);
-    conv3(c, F(D), ga, C, nD, nbr(D), dp.a, 0, nullptr, nullptr, 0, nullptr, hx);
-    dbgF(nm("hx", d), hx, nD, C);
-    conv3(c, hx, nullptr, C, nD, nbr(D), dp.b, 2, F(D), ga, 0, dp.P, Hk);
+    if (m->flags & MF_XFP_OFF) {
+      // "Baseline + GRED" (Table 4): H = ResBlock(G_D), no cross-scale concat
+      conv3(c, ga, nullptr, C, nD, nbr(D), dp.a, 0, nullptr, nullptr, 0, nullptr, hx);
+      dbgF(nm("hx", d), hx, nD, C);
+      conv3(c, hx, nullptr, C, nD, nbr(D), dp.b, 1, ga, nullptr, dp.k_s, nullptr, Hk);
+    } else {
+      // Eq.10: H = ResBlock(Concat(F_D, G_D)), virtual concat, 1x1 projection skip
+      conv3(c, F(D), ga, C, nD, nbr(D), dp.a, 0, nullptr, nullptr, 0, nullptr, hx);
+      dbgF(nm("hx", d), hx, nD, C);
+      conv3(c, hx, nullptr, C, nD, nbr(D), dp.b, 2, F(D), ga, 0, dp.P, Hk);
+    }
     dbgF(nm("H", d), Hk, nD, C);
     // Eq.11: up/prune chain D -> d (H at k = D only, reading Q3)
     size_t mx = 0;
@@ -493,12 +526,13 @@ struct Net {
 // encoder output packing (reading O11)
 // ============================================================================
 __global__ void k_pack_sizes(const PackItem* __restrict__ items, int n, const EncSeg* __restrict__ segs,
-                             const uint32_t* __restrict__ seg_W, uint32_t* __restrict__ sizes) {
+                             const uint32_t* __restrict__ seg_W, const uint32_t* __restrict__ raw_sz,
+                             uint32_t* __restrict__ sizes) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const PackItem it = items[i];
   if (it.kind == 0) {
-    sizes[i] = it.bytes;
+    sizes[i] = it.bytes + ((raw_sz[it.frame] + 3u) & ~3u);  // header + level sizes + padded raw region
   } else {
     const uint32_t ns = segs[it.seg].n;
     uint32_t k = (ns + 511u) / 512u;
@@ -510,9 +544,10 @@ __global__ void k_pack_sizes(const PackItem* __restrict__ items, int n, const En
 __global__ void k_pack_write(const PackItem* __restrict__ items, int n, const uint32_t* __restrict__ item_off,
                              const uint32_t* __restrict__ sizes, const EncSeg* __restrict__ segs,
                              const uint32_t* __restrict__ seg_W, const uint32_t* __restrict__ seg_state,
-                             const uint16_t* __restrict__ words, int L, int R, int n_deep, uint64_t hash,
-                             const uint32_t* __restrict__ foff, int B, const uint64_t* __restrict__ nb,
-                             const uint8_t* __restrict__ code, uint8_t* __restrict__ out) {
+                             const uint16_t* __restrict__ words, int L, int R, int n_deep, uint32_t flags,
+                             uint64_t hash, const uint32_t* __restrict__ foff, int B, const uint64_t* __restrict__ nb,
+                             const uint8_t* __restrict__ code, const uint32_t* __restrict__ raw_sz,
+                             const uint8_t* __restrict__ raw_region, uint32_t raw_cap, uint8_t* __restrict__ out) {
   const int i = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= n) return;
@@ -520,13 +555,12 @@ __global__ void k_pack_write(const PackItem* __restrict__ items, int n, const ui
   uint8_t* o = out + item_off[i];
   if (it.kind == 0) {
     const int f = int(it.frame);
-    uint32_t raw = 0;
-    for (int d = 0; d < R; ++d) raw += foff[d * (B + 1) + f + 1] - foff[d * (B + 1) + f];
+    const uint32_t raw = raw_sz[f];
     const uint32_t NL = foff[L * (B + 1) + f + 1] - foff[L * (B + 1) + f];
     if (lane == 0) {
       o[0] = 'P'; o[1] = 'C'; o[2] = 'C'; o[3] = '1';
       o[4] = 1; o[5] = 0;
-      o[6] = uint8_t(L); o[7] = uint8_t(R); o[8] = uint8_t(n_deep); o[9] = 0;
+      o[6] = uint8_t(L); o[7] = uint8_t(R); o[8] = uint8_t(n_deep); o[9] = uint8_t(flags);
       o[10] = uint8_t(raw); o[11] = uint8_t(raw >> 8);
       for (int b = 0; b < 4; ++b) o[12 + b] = uint8_t(NL >> (8 * b));
       for (int b = 0; b < 8; ++b) o[16 + b] = uint8_t(hash >> (8 * b));
@@ -539,13 +573,20 @@ __global__ void k_pack_write(const PackItem* __restrict__ items, int n, const ui
       uint8_t* q = o + 24 + 4 * (d - R);
       q[0] = uint8_t(s); q[1] = uint8_t(s >> 8); q[2] = uint8_t(s >> 16); q[3] = uint8_t(s >> 24);
     }
-    // raw prefix X_0..X_{R-1} (reading Q13), zero-padded to 4 bytes
+    // raw prefix X_0..X_{R-1}: plain bytes (reading Q13) or the frequency-coded region
+    // (MF_RAW_FREQ), zero-padded to 4 bytes
     uint8_t* rp = o + 24 + 4 * (L - R);
     uint32_t pos = 0;
-    for (int d = 0; d < R; ++d) {
-      const uint32_t a = foff[d * (B + 1) + f], cnt = foff[d * (B + 1) + f + 1] - a;
-      for (uint32_t k = lane; k < cnt; k += 32) rp[pos + k] = code[nb[d] + a + k];
-      pos += cnt;
+    if (raw_region) {
+      const uint8_t* src = raw_region + size_t(f) * raw_cap;
+      for (uint32_t k = lane; k < raw; k += 32) rp[k] = src[k];
+      pos = raw;
+    } else {
+      for (int d = 0; d < R; ++d) {
+        const uint32_t a = foff[d * (B + 1) + f], cnt = foff[d * (B + 1) + f + 1] - a;
+        for (uint32_t k = lane; k < cnt; k += 32) rp[pos + k] = code[nb[d] + a + k];
+        pos += cnt;
+      }
     }
     for (uint32_t k = pos + lane; k < ((pos + 3u) & ~3u); k += 32) rp[k] = 0;
   } else {
@@ -591,12 +632,15 @@ __global__ void k_raw_count(const uint8_t* __restrict__ bs, const uint64_t* __re
   if (bad) atomicOr(err, EF_CORRUPT);
 }
 
-__global__ void k_raw_write(const uint8_t* __restrict__ bs, const uint64_t* __restrict__ raw_off, int B, int R,
-                            const uint32_t* __restrict__ foff, const uint64_t* __restrict__ nb, uint64_t* __restrict__ key,
-                            uint8_t* __restrict__ code, uint32_t* __restrict__ cs, uint32_t* __restrict__ par) {
+// src: the bitstream with per-frame raw offsets (plain bytes), or, when stride != 0, the
+// frequency decoder's symbols at src + f * stride
+__global__ void k_raw_write(const uint8_t* __restrict__ bs, const uint64_t* __restrict__ raw_off, uint32_t stride, int B,
+                            int R, const uint32_t* __restrict__ foff, const uint64_t* __restrict__ nb,
+                            uint64_t* __restrict__ key, uint8_t* __restrict__ code, uint32_t* __restrict__ cs,
+                            uint32_t* __restrict__ par) {
   int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= B) return;
-  const uint8_t* p = bs + raw_off[f];
+  const uint8_t* p = stride ? bs + size_t(f) * stride : bs + raw_off[f];
   key[nb[0] + f] = uint64_t(f);
   uint32_t pos = 0;
   for (int d = 0; d < R; ++d) {
@@ -679,9 +723,7 @@ void encode_batch(pcc_ctx c, pcc_model m, const int32_t* d_xyz, const size_t* of
   std::vector<PackItem> items;
   for (int f = 0; f < B; ++f) {
     const size_t i0 = items.size();
-    uint32_t raw = 0;
-    for (int d = 0; d < R; ++d) raw += o.foff[size_t(d) * (B + 1) + f + 1] - o.foff[size_t(d) * (B + 1) + f];
-    items.push_back(PackItem{0, uint32_t(f), 0, 0, uint32_t(24 + 4 * (L - R) + ((raw + 3) & ~3u)), 0});
+    items.push_back(PackItem{0, uint32_t(f), 0, 0, uint32_t(24 + 4 * (L - R)), 0});
     for (int d = R; d < L; ++d) {
       const uint32_t a = o.foff[size_t(d) * (B + 1) + f], nfd = o.foff[size_t(d) * (B + 1) + f + 1] - a;
       for (uint32_t s0 = 0; s0 < nfd; s0 += SEG_SYMS) {
@@ -700,9 +742,17 @@ void encode_batch(pcc_ctx c, pcc_model m, const int32_t* d_xyz, const size_t* of
   rans_encode(c, d_segs, nseg, cf, words, seg_W, seg_state);
   uint32_t* sizes = buf<uint32_t>(c, "item_sizes", nit + 1);
   uint32_t* ioff = buf<uint32_t>(c, "item_off", nit + 1);
+  uint64_t* d_nb = upload(c, "nb", o.nb);
+  uint32_t* d_foff = static_cast<uint32_t*>(c->bufs.at("foff").p);
+  // raw prefix region per frame (plain bytes, or the P:601 frequency coder)
+  const bool rawfreq = (m->flags & MF_RAW_FREQ) != 0;
+  const uint32_t raw_cap = (8u + 2u * raw_max_symbols(R) + 4u + 3u) & ~3u;
+  uint8_t* raw_region = rawfreq ? buf<uint8_t>(c, "raw_region", size_t(B) * raw_cap) : nullptr;
+  uint32_t* raw_sz = buf<uint32_t>(c, "raw_sz", B);
+  raw_encode(c, rawfreq, static_cast<uint8_t*>(c->bufs.at("code").p), d_nb, d_foff, B, R, raw_region, raw_cap, raw_sz);
   {
     Prof p(c, "pack", 0);
-    k_pack_sizes<<<cdiv(nit, 128), 128, 0, s>>>(d_items, nit, d_segs, seg_W, sizes);
+    k_pack_sizes<<<cdiv(nit, 128), 128, 0, s>>>(d_items, nit, d_segs, seg_W, raw_sz, sizes);
     launched(c);
   }
   scan_u32(c, sizes, ioff, size_t(nit));
@@ -719,12 +769,11 @@ void encode_batch(pcc_ctx c, pcc_model m, const int32_t* d_xyz, const size_t* of
     out_offs[B] = total;
   }
   if (total > out_cap || !d_out) throw Error{PCC_ERR_CAPACITY};
-  uint64_t* d_nb = upload(c, "nb", o.nb);
   Prof pw(c, "pack", total);
   k_pack_write<<<cdiv(size_t(nit) * 32, 128), 128, 0, s>>>(d_items, nit, ioff, sizes, d_segs, seg_W, seg_state, words, L,
-                                                          R, m->n_deep, m->hash,
-                                                          static_cast<uint32_t*>(c->bufs.at("foff").p), B, d_nb,
-                                                          static_cast<uint8_t*>(c->bufs.at("code").p), d_out);
+                                                          R, m->n_deep, m->flags, m->hash, d_foff, B, d_nb,
+                                                          static_cast<uint8_t*>(c->bufs.at("code").p), raw_sz,
+                                                          raw_region, raw_cap, d_out);
   launched(c);
   PCC_CUDA(cudaStreamSynchronize(s));
   PCC_CUDA(cudaGetLastError());
@@ -778,7 +827,7 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
     x.raw = uint32_t(h[10]) | uint32_t(h[11]) << 8;
     std::memcpy(&x.NL, h + 12, 4);
     std::memcpy(&x.hash, h + 16, 8);
-    if (x.hash != m->hash || x.R != m->R || x.nd != m->n_deep) throw Error{PCC_ERR_MODEL_MISMATCH};
+    if (x.hash != m->hash || x.R != m->R || x.nd != m->n_deep || h[9] != m->flags) throw Error{PCC_ERR_MODEL_MISMATCH};
     check_depth(m, x.L);
     if (x.L != hd[0].L) throw Error{PCC_ERR_INVALID_ARG};  // a batch shares one bit depth
     if (len[f] < size_t(24 + 4 * (x.L - x.R))) throw Error{PCC_ERR_TRUNCATED};
@@ -828,7 +877,15 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
   uint64_t* d_raw_off = upload(c, "d_raw_off", raw_off);
   uint32_t* d_raw_len = upload(c, "d_raw_len", raw_len);
   uint32_t* d_cnt = buf<uint32_t>(c, "raw_cnt", size_t(B) * (R + 1));
-  {
+  const bool rawfreq = (m->flags & MF_RAW_FREQ) != 0;
+  uint8_t* raw_sym = nullptr;
+  if (rawfreq) {  // P:601 frequency-coded raw prefix: decode the symbols first
+    std::vector<uint32_t> nl(B);
+    for (int f = 0; f < B; ++f) nl[f] = hd[f].NL;
+    uint32_t* d_nl = upload(c, "d_raw_nl", nl);
+    raw_sym = buf<uint8_t>(c, "raw_sym", size_t(B) * raw_max_symbols(R));
+    raw_decode(c, d_bs, d_raw_off, d_raw_len, B, R, d_nl, raw_sym, d_cnt, err);
+  } else {
     Prof p(c, "container", 0);
     k_raw_count<<<cdiv(B, 128), 128, 0, s>>>(d_bs, d_raw_off, d_raw_len, B, R, d_cnt, err);
     launched(c);
@@ -860,7 +917,8 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
   uint64_t* d_nb = upload(c, "nb", o.nb);
   {
     Prof praw(c, "container", 0);
-    k_raw_write<<<cdiv(B, 128), 128, 0, s>>>(d_bs, d_raw_off, B, R, d_foff, d_nb,
+    k_raw_write<<<cdiv(B, 128), 128, 0, s>>>(rawfreq ? raw_sym : d_bs, d_raw_off, rawfreq ? raw_max_symbols(R) : 0u, B,
+                                             R, d_foff, d_nb,
                                              static_cast<uint64_t*>(c->bufs.at("key").p),
                                              static_cast<uint8_t*>(c->bufs.at("code").p),
                                              static_cast<uint32_t*>(c->bufs.at("cs").p),
@@ -912,6 +970,14 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
   PCC_CUDA(cudaGetLastError());
 }
 
+// Frames coded together carry their index above the 3L Morton bits of a u64 key.  At
+// most 2^fb - 1 frames share a launch, so no key (frame 2^fb - 1's corner voxel would be
+// all ones) equals the kernel-map hash's EMPTY sentinel ~0.
+int frames_per_chunk(int frames, int fb_max) {
+  if (fb_max >= 30) return frames;
+  return std::max(1, std::min(frames, (1 << fb_max) - 1));
+}
+
 template <class F>
 pcc_status guard(pcc_ctx c, F&& f) {
   try {
@@ -940,6 +1006,41 @@ pcc_status pcc_model_load(const void* bytes, size_t len, int device, pcc_model* 
     check_device(device);
     *out = load_model(static_cast<const uint8_t*>(bytes), len, device);
   });
+}
+
+pcc_status pcc_model_random_file(const pcc_model_config* cfg, void* buf, size_t cap, size_t* len) {
+  if (!cfg || !len) return PCC_ERR_INVALID_ARG;
+  return guard(nullptr, [&] {
+    if (!model_config_valid(*cfg)) throw Error{PCC_ERR_INVALID_ARG};
+    const std::vector<uint8_t> f = random_model_file(*cfg);
+    *len = f.size();
+    if (!buf || cap < f.size()) throw Error{PCC_ERR_CAPACITY};
+    std::memcpy(buf, f.data(), f.size());
+  });
+}
+
+pcc_status pcc_model_create_random(const pcc_model_config* cfg, int device, pcc_model* out) {
+  if (!cfg || !out) return PCC_ERR_INVALID_ARG;
+  return guard(nullptr, [&] {
+    if (!model_config_valid(*cfg)) throw Error{PCC_ERR_INVALID_ARG};
+    check_device(device);
+    const std::vector<uint8_t> f = random_model_file(*cfg);
+    *out = load_model(f.data(), f.size(), device);
+  });
+}
+
+pcc_status pcc_model_save(pcc_model m, void* buf, size_t cap, size_t* len) {
+  if (!m || !len) return PCC_ERR_INVALID_ARG;
+  *len = m->file.size();
+  if (!buf || cap < m->file.size()) return PCC_ERR_CAPACITY;
+  std::memcpy(buf, m->file.data(), m->file.size());
+  return PCC_OK;
+}
+
+pcc_status pcc_model_flags(pcc_model m, uint32_t* out) {
+  if (!m || !out) return PCC_ERR_INVALID_ARG;
+  *out = m->flags;
+  return PCC_OK;
 }
 
 pcc_status pcc_model_hash(pcc_model m, uint64_t* out) {
@@ -1035,7 +1136,7 @@ pcc_status pcc_hrcs_stats(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, i
     if (!d_xyz) throw Error{PCC_ERR_INVALID_ARG};
     PCC_CUDA(cudaSetDevice(c->device));
     const int L = bit_depth, fb_max = 64 - 3 * L;
-    const int chunk = fb_max >= 30 ? frames : std::max(1, std::min(frames, 1 << fb_max));
+    const int chunk = frames_per_chunk(frames, fb_max);
     std::vector<uint64_t> res(size_t(chunk) * (L + 1));
     std::vector<size_t> sub;
     for (int f0 = 0; f0 < frames; f0 += chunk) {
@@ -1065,7 +1166,7 @@ pcc_status pcc_encode_batch(pcc_ctx c, pcc_model m, const int32_t* d_xyz, const 
     if (!c || !m || !offs || !out_offs || frames < 1) throw Error{PCC_ERR_INVALID_ARG};
     check_depth(m, bit_depth);
     const int fb_max = 64 - 3 * bit_depth;
-    const int chunk = fb_max >= 30 ? frames : std::max(1, std::min(frames, 1 << fb_max));
+    const int chunk = frames_per_chunk(frames, fb_max);
     size_t base_out = 0;
     std::vector<size_t> sub_offs, sub_out;
     for (int f0 = 0; f0 < frames; f0 += chunk) {

@@ -179,12 +179,8 @@ __global__ void __launch_bounds__(UNT, 1) k_up_tc(const int8_t* __restrict__ S, 
 void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* par_c, const uint64_t* key_c,
                  uint32_t nc, const DUp& L, int8_t* out) {
   constexpr int smem = SM_END;  // ~207 KB: one CTA (four tile groups) per SM
-  static bool attr = false;
-  if (!attr) {
-    PCC_CUDA(cudaFuncSetAttribute(k_up_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    PCC_CUDA(cudaFuncSetAttribute(k_up_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  PCC_SMEM_ATTR(k_up_tc<true>, smem);
+  PCC_SMEM_ATTR(k_up_tc<false>, smem);
   const uint32_t ntiles = (nc + 127) / 128;
   const unsigned grid = std::max(1u, std::min((ntiles + UG - 1) / UG, unsigned(c->sm_count)));
   Prof p(c, "up", size_t(nc) * (4 + 8 + 2 * 32));

@@ -22,6 +22,22 @@ STATUS = ["OK", "INVALID_ARG", "EMPTY", "RANGE", "UNSUPPORTED_DEPTH", "CAPACITY"
           "MODEL_MISMATCH", "TRUNCATED", "CORRUPT", "CUDA", "OOM"]
 
 
+MODEL_XFP_OFF = 1   # PCC_MODEL_XFP_OFF
+MODEL_RAW_FREQ = 2  # PCC_MODEL_RAW_FREQ
+
+
+class ModelConfig(ct.Structure):
+    """pcc_model_config (include/pcc.h)."""
+    _fields_ = [("channels", ct.c_int), ("head_hidden", ct.c_int), ("raw_levels", ct.c_int), ("deep_levels", ct.c_int),
+                ("min_depth", ct.c_int), ("max_depth", ct.c_int), ("seed", ct.c_uint64), ("flags", ct.c_uint32)]
+
+
+def model_config(channels=32, head_hidden=None, raw_levels=4, deep_levels=4, min_depth=9, max_depth=18, seed=1,
+                 flags=0) -> ModelConfig:
+    return ModelConfig(channels, channels if head_hidden is None else head_hidden, raw_levels, deep_levels, min_depth,
+                       max_depth, seed, flags)
+
+
 class PCCError(RuntimeError):
     def __init__(self, status: int, where: str = ""):
         self.status = status
@@ -37,6 +53,10 @@ def _load():
     SP = ct.POINTER(ct.c_size_t)
     L.pcc_model_load.argtypes = [P, S, I, ct.POINTER(P)]
     L.pcc_model_hash.argtypes = [P, ct.POINTER(U64)]
+    L.pcc_model_flags.argtypes = [P, ct.POINTER(ct.c_uint32)]
+    L.pcc_model_create_random.argtypes = [ct.POINTER(ModelConfig), I, ct.POINTER(P)]
+    L.pcc_model_random_file.argtypes = [ct.POINTER(ModelConfig), P, S, SP]
+    L.pcc_model_save.argtypes = [P, P, S, SP]
     L.pcc_model_info.argtypes = [P] + [ct.POINTER(I)] * 6
     L.pcc_model_destroy.argtypes = [P]
     L.pcc_ctx_create.argtypes = [I, P, ct.POINTER(P)]
@@ -65,7 +85,8 @@ def _load():
     L.pcc_debug_gemm_i8.restype = I
     L.pcc_status_string.argtypes = [I]
     L.pcc_status_string.restype = ct.c_char_p
-    for f in ("pcc_model_load", "pcc_model_hash", "pcc_model_info", "pcc_ctx_create", "pcc_build_octree", "pcc_hrcs_stats",
+    for f in ("pcc_model_load", "pcc_model_hash", "pcc_model_info", "pcc_model_flags", "pcc_model_create_random",
+              "pcc_model_random_file", "pcc_model_save", "pcc_ctx_create", "pcc_build_octree", "pcc_hrcs_stats",
               "pcc_encode", "pcc_decode", "pcc_encode_batch", "pcc_decode_batch", "pcc_encode_batch_host",
               "pcc_decode_batch_host", "pcc_debug_tensor", "pcc_ctx_set_debug"):
         getattr(L, f).restype = I
@@ -74,7 +95,8 @@ def _load():
 
 lib = _load()
 
-EXPORTS = ("pcc_model_load", "pcc_model_hash", "pcc_model_info", "pcc_model_destroy", "pcc_ctx_create",
+EXPORTS = ("pcc_model_load", "pcc_model_create_random", "pcc_model_random_file", "pcc_model_save", "pcc_model_hash",
+           "pcc_model_flags", "pcc_model_info", "pcc_model_destroy", "pcc_ctx_create",
            "pcc_ctx_destroy", "pcc_encode_bound", "pcc_build_octree", "pcc_hrcs_stats", "pcc_encode", "pcc_decode",
            "pcc_encode_batch", "pcc_decode_batch", "pcc_encode_batch_host", "pcc_decode_batch_host",
            "pcc_debug_tensor", "pcc_ctx_set_debug", "pcc_ctx_launch_count", "pcc_ctx_set_profile",
@@ -110,6 +132,34 @@ def pcc_model_load(model_bytes: bytes, device: int = 0) -> ct.c_void_p:
     buf = ct.create_string_buffer(model_bytes, len(model_bytes))
     _chk(lib.pcc_model_load(buf, len(model_bytes), device, ct.byref(h)), "pcc_model_load")
     return h
+
+
+def pcc_model_create_random(cfg: ModelConfig, device: int = 0) -> ct.c_void_p:
+    h = ct.c_void_p()
+    _chk(lib.pcc_model_create_random(ct.byref(cfg), device, ct.byref(h)), "pcc_model_create_random")
+    return h
+
+
+def pcc_model_random_file(cfg: ModelConfig) -> bytes:
+    n = ct.c_size_t()
+    _chk(lib.pcc_model_random_file(ct.byref(cfg), None, 0, ct.byref(n)), "pcc_model_random_file", ok=(0, 5))
+    buf = ct.create_string_buffer(n.value)
+    _chk(lib.pcc_model_random_file(ct.byref(cfg), buf, n.value, ct.byref(n)), "pcc_model_random_file")
+    return buf.raw[:n.value]
+
+
+def pcc_model_save(m) -> bytes:
+    n = ct.c_size_t()
+    _chk(lib.pcc_model_save(m, None, 0, ct.byref(n)), "pcc_model_save", ok=(0, 5))
+    buf = ct.create_string_buffer(n.value)
+    _chk(lib.pcc_model_save(m, buf, n.value, ct.byref(n)), "pcc_model_save")
+    return buf.raw[:n.value]
+
+
+def pcc_model_flags(m) -> int:
+    v = ct.c_uint32()
+    _chk(lib.pcc_model_flags(m, ct.byref(v)), "pcc_model_flags")
+    return v.value
 
 
 def pcc_model_hash(m) -> int:

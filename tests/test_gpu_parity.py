@@ -183,6 +183,29 @@ def test_encoder_per_tensor_parity(pcc, ctx, C, cfg):
     assert got[0] == want
 
 
+def check_decoder_rows(pcc, ctx, D, d):
+    """The decoder rows of level d (DESIGN.md §5 "Data layout") rebuild exactly the
+    oracle's cumulative bounds C_i = i + floor(E_i 65281 / S) (reading Q21), and the
+    decoded codes are the oracle's."""
+    p = D.get(f"p/{d}", np.uint16).reshape(-1, 255).astype(np.int64)
+    cum = np.concatenate([np.zeros((p.shape[0], 1), np.int64), np.cumsum(p, 1)[:, :254]], 1)
+    raw = pcc.pcc_debug_tensor(ctx, f"cdf/{d}")
+    hdr = np.frombuffer(raw, np.uint32).reshape(-1, 148)[:, :20].astype(np.int64)
+    j = np.frombuffer(raw, np.uint16).reshape(-1, 296)[:, 40:40 + 255].astype(np.int64)
+    # decoder row: S, floor(65281 2^32 / S), E_{16k}, then the LUT index of every symbol
+    lut = np.concatenate([I.exp_lut().astype(np.int64), [0]])
+    e = lut[j]
+    E = np.concatenate([np.zeros((e.shape[0], 1), np.int64), np.cumsum(e, 1)], 1)
+    S = hdr[:, 0]
+    assert np.array_equal(E[:, 255], S), d
+    assert np.array_equal(hdr[:, 1], (65281 << 32) // S), d
+    assert np.array_equal(hdr[:, 2:17], E[:, 16:241:16]), d
+    C = np.arange(255)[None, :] + (E[:, :255] * 65281) // S[:, None]
+    assert np.array_equal(C, cum), d
+    assert np.array_equal(np.frombuffer(pcc.pcc_debug_tensor(ctx, f"code/{d}"), np.uint8),
+                          D.get(f"code/{d}", np.uint8)), d
+
+
 def test_decoder_cdf_parity(pcc, ctx):
     mb, om = model_pair(8)
     m = gpu_model(pcc, mb)
@@ -193,24 +216,7 @@ def test_decoder_cdf_parity(pcc, ctx):
     try:
         out = gpu_decode(pcc, ctx, m, [bs], len(pts))
         for d in range(4, 12):
-            p = D.get(f"p/{d}", np.uint16).reshape(-1, 255).astype(np.int64)
-            cum = np.concatenate([np.zeros((p.shape[0], 1), np.int64), np.cumsum(p, 1)[:, :254]], 1)
-            raw = pcc.pcc_debug_tensor(ctx, f"cdf/{d}")
-            hdr = np.frombuffer(raw, np.uint32).reshape(-1, 148)[:, :20].astype(np.int64)
-            j = np.frombuffer(raw, np.uint16).reshape(-1, 296)[:, 40:40 + 255].astype(np.int64)
-            # decoder row: S, floor(65281 2^32 / S), E_{16k}, then the LUT
-            # index of every symbol; C_i = i + floor(E_i 65281 / S) must be the oracle's
-            lut = np.concatenate([I.exp_lut().astype(np.int64), [0]])
-            e = lut[j]
-            E = np.concatenate([np.zeros((e.shape[0], 1), np.int64), np.cumsum(e, 1)], 1)
-            S = hdr[:, 0]
-            assert np.array_equal(E[:, 255], S), d
-            assert np.array_equal(hdr[:, 1], (65281 << 32) // S), d
-            assert np.array_equal(hdr[:, 2:17], E[:, 16:241:16]), d
-            C = np.arange(255)[None, :] + (E[:, :255] * 65281) // S[:, None]
-            assert np.array_equal(C, cum), d
-            assert np.array_equal(np.frombuffer(pcc.pcc_debug_tensor(ctx, f"code/{d}"), np.uint8),
-                                  D.get(f"code/{d}", np.uint8)), d
+            check_decoder_rows(pcc, ctx, D, d)
     finally:
         pcc.pcc_ctx_set_debug(ctx, False)
     assert np.array_equal(out[0], morton_sorted_unique(pts, 12))
