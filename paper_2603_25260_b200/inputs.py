@@ -34,6 +34,7 @@ GROUND_Z = -1.73          # sensor height above ground (KITTI HDL-64E mount), SU
 MAX_RANGE = 120.0
 RING_RADIUS = 60.0
 RING_TOP = 30.0 + GROUND_Z
+SCENE_PERIOD = 160.0      # box layout period along the road (x), metres
 
 
 @dataclasses.dataclass(frozen=True)
@@ -99,10 +100,15 @@ def raycast_frame(cfg: ScanConfig, frame_index: int = 0, scene_seed: int = 1,
     zr = tr * d[:, 2]
     ok = (zr >= GROUND_Z) & (zr <= RING_TOP)
     t = np.where(ok & (tr < t), tr, t)
-    # boxes (slab test), translated into the sensor frame
+    # boxes (slab test), translated into the sensor frame.  The street scene tiles along
+    # the road with period SCENE_PERIOD: every box copy is placed within +-80 m of the
+    # sensor along x, so every frame of a long sequence (cfg5: 1000 frames, 1 m apart)
+    # sees a full scene of objects, not the empty road beyond the first tile
     boxes = _scene_boxes(scene_seed).copy()
-    boxes[:, 0] -= float(frame_index)
-    boxes[:, 3] -= float(frame_index)
+    cx = 0.5 * (boxes[:, 0] + boxes[:, 3]) - float(frame_index)
+    shift = np.floor((cx + SCENE_PERIOD / 2.0) / SCENE_PERIOD) * SCENE_PERIOD + float(frame_index)
+    boxes[:, 0] -= shift
+    boxes[:, 3] -= shift
     inv = 1.0 / np.where(np.abs(d) < 1e-12, 1e-12, d)
     inv3 = inv.reshape(cfg.beams, cfg.azimuths, 3)
     t2d = t.reshape(cfg.beams, cfg.azimuths)

@@ -1,18 +1,17 @@
-"""NEXT-2: float twin of the occupancy head and the decode-collapse demo.
+"""NEXT-2: whole-network float twin and the cross-platform decode collapse.
 
-The paper's motivation (Fig.2b/c): a floating-point entropy model is
-not bit-reproducible across devices / evaluation orders, and an arithmetic decoder fed a
-CDF that differs from the encoder's in a single entry decodes garbage from there on; the
-integer-only model is exact everywhere (our GPU path reproduces the oracle's CDFs and
-bitstreams bit for bit: tests/test_gpu_parity.py).
+P:85-99 (Fig. 2b): encoding on one GPU and decoding on another with floating-point
+inference "collapses into an approximately uniform distribution"; Fig. 2c / P:287-290:
+integer-only inference decodes bit-exactly.  tests/float_twin.py builds the float32 twin
+of the ENTIRE integer network (every layer, not only the predictor) and codes with it.
 
-Float twin (same weights, dequantised): a = PReLU(W1 F + b1) with slopes m_pos / 2^r and
-m_neg / 2^r (the requant multipliers without rounding or clipping); z = W2 a + b2; logits
-in nats l = z m_l / 2^r_l / 256 (Q8 -> nats, reading Q20); pmf p = softmax(l) quantised
-like reading Q21: 1 + floor(p * 65281), leftover to the first argmax.  Two evaluation
-orders stand in for two devices: float32 BLAS matmul vs float32 accumulation in reversed
-order (and, on a GPU box, torch fp32 on cuda:0).  The rANS coder here is the single-lane
-form of reading O9 (32-bit state, 16-bit words, M = 2^16).
+* the twin is the same network: its logits track the integer model's (correlation);
+* same backend and order: float encode -> float decode is lossless;
+* another evaluation order (CPU) or another device (GPU fp32 vs CPU fp32): some node
+  CDFs differ, the decoder derails at the first differing node of a level, and the
+  decoded cloud is not the input (asserted);
+* the integer path is identical across devices: GPU encode -> oracle (CPU) decode and
+  oracle encode -> GPU decode are both exact (asserted on a GPU box).
 """
 import numpy as np
 import pytest
@@ -20,140 +19,108 @@ import pytest
 from oracle import oracle as O
 from paper_2603_25260_b200 import inputs as I
 
-M = 1 << 16
+from float_twin import FloatTwin, float_decode, float_encode, quantise_pmf, rans_decode, rans_encode
 
-
-def _head_inputs(model_obj, D, d, Dcut):
-    F = D.get(f"F/{d}" if d <= Dcut else f"Fp/{d}/{d}", np.int8)
-    hd = model_obj.shallow[d].head if d <= Dcut else model_obj.deep[d - Dcut - 1].head
-    return F.reshape(-1, model_obj.C), hd
-
-
-def float_logits(F, hd, order):
-    """Float twin of Eq.7's predictor: nats, float32, evaluated in `order`."""
-    f32 = np.float32
-    W1, b1, W2, b2 = hd.W1.astype(f32), hd.b1.astype(f32), hd.W2.astype(f32), hd.b2.astype(f32)
-    Fx = F.astype(f32)
-    if order == "blas":
-        h = Fx @ W1.T + b1
-    else:  # reversed accumulation order, one float32 add at a time
-        h = np.zeros((F.shape[0], W1.shape[0]), f32)
-        for c in reversed(range(W1.shape[1])):
-            h = (h + Fx[:, c:c + 1] * W1[None, :, c]).astype(f32)
-        h = (h + b1).astype(f32)
-    sp, sn = f32(hd.rq1.m_pos / 2.0 ** hd.rq1.r), f32(hd.rq1.m_neg / 2.0 ** hd.rq1.r)
-    a = np.where(h >= 0, h * sp, h * sn).astype(f32)
-    if order == "blas":
-        z = a @ W2.T + b2
-    else:
-        z = np.zeros((F.shape[0], W2.shape[0]), f32)
-        for k in reversed(range(W2.shape[1])):
-            z = (z + a[:, k:k + 1] * W2[None, :, k]).astype(f32)
-        z = (z + b2).astype(f32)
-    return (z * f32(hd.rq_logit.m_pos / 2.0 ** hd.rq_logit.r / 256.0)).astype(f32)
-
-
-def quantise_pmf(logits):
-    """softmax in float32, then reading Q21's quantiser (every p >= 1, sum 2^16)."""
-    l = logits.astype(np.float32)
-    e = np.exp(l - l.max(1, keepdims=True)).astype(np.float32)
-    pr = (e / e.sum(1, keepdims=True)).astype(np.float32)
-    p = 1 + np.floor(pr * np.float32(65281)).astype(np.int64)
-    p[np.arange(len(p)), np.argmax(p, 1)] += M - p.sum(1)
-    return p
-
-
-def rans_encode(sym, pmfs):
-    """Reading O9, one lane: returns (words, final state); sym in 0..254."""
-    cum = np.concatenate([np.zeros((len(pmfs), 1), np.int64), np.cumsum(pmfs, 1)], 1)
-    x, words = 1 << 16, []
-    for i in reversed(range(len(sym))):
-        s = int(sym[i])
-        f, c = int(pmfs[i, s]), int(cum[i, s])
-        if x >= f << 16:
-            words.append(x & 0xFFFF)
-            x >>= 16
-        x = ((x // f) << 16) + (x % f) + c
-    return words[::-1], x
-
-
-def rans_decode(words, x, pmfs):
-    cum = np.concatenate([np.zeros((len(pmfs), 1), np.int64), np.cumsum(pmfs, 1)], 1)
-    out, w = [], 0
-    for i in range(len(pmfs)):
-        slot = x & 0xFFFF
-        s = int(np.searchsorted(cum[i], slot, side="right") - 1)
-        s = min(max(s, 0), 254)
-        out.append(s)
-        x = int(pmfs[i, s]) * (x >> 16) + slot - int(cum[i, s])
-        if x < (1 << 16) and w < len(words):
-            x = (x << 16) | words[w]
-            w += 1
-    return np.array(out)
+L = 12
 
 
 @pytest.fixture(scope="module")
-def level_data():
-    mobj = I.make_model(C=8, H=8, seed=1, min_depth=9, max_depth=12)
-    om = O.Model(mobj.to_bytes())
+def setup():
+    model = I.make_model(C=8, H=8, seed=1, min_depth=9, max_depth=12)
+    pts = I.make_frame(I.CFG1, 3)
+    keys, _ = O.build_octree(pts, L)
+    return model, pts, keys[L]
+
+
+@pytest.fixture(scope="module")
+def cpu_stream(setup):
+    model, pts, _ = setup
+    return float_encode(FloatTwin(model, "cpu", "fused"), pts, L)
+
+
+def test_quantiser_and_coder():
+    rng = np.random.default_rng(0)
+    lg = rng.normal(0, 2, size=(500, 255)).astype(np.float32)
+    p = quantise_pmf(lg)
+    assert (p >= 1).all() and (p.sum(1) == 1 << 16).all()
+    sym = rng.integers(0, 255, size=500)
+    w, x = rans_encode(sym, p)
+    assert np.array_equal(rans_decode(w, x, p)[0], sym)
+
+
+def test_twin_is_the_same_network(setup):
+    """The twin's logits track the integer model's on the same (integer) octree: the
+    integer z/d dumps (Eq.7) and the twin's float logits correlate strongly per level."""
+    model, pts, _ = setup
+    om = O.Model(model.to_bytes())
     D = O.Dump()
-    O.encode(om, I.make_frame(I.CFG1), 12, D)
-    Dcut = 12 - 1 - mobj.n_deep
-    out = []
-    for d in range(mobj.R, 12):
-        F, hd = _head_inputs(mobj, D, d, Dcut)
-        sym = D.get(f"code/{d}", np.uint8).astype(np.int64) - 1
-        p_int = D.get(f"p/{d}", np.uint16).reshape(-1, 255).astype(np.int64)
-        out.append((d, F, hd, sym, p_int))
-    return out
+    O.encode(om, pts, L, D)
+    keys, codes = O.build_octree(pts, L)
+    tw = FloatTwin(model, "cpu", "fused")
+    tw.reset()
+    for d in range(model.R, L):
+        p_f = tw.level_pmf(keys, codes, d, L)
+        p_i = D.get(f"p/{d}", np.uint16).reshape(-1, 255).astype(np.float64)
+        lf, li = np.log(p_f.astype(np.float64)), np.log(p_i)
+        r = np.corrcoef(lf.ravel(), li.ravel())[0, 1]
+        assert r > 0.9, (d, r)
 
 
-def test_integer_pmfs_round_trip(level_data):
-    """The integer model's pmfs (identical on CPU oracle and GPU) always decode."""
-    for d, F, hd, sym, p_int in level_data:
-        assert (p_int >= 1).all() and (p_int.sum(1) == M).all()
-        words, x = rans_encode(sym, p_int)
-        assert np.array_equal(rans_decode(words, x, p_int), sym), d
+def test_float_same_order_round_trip(setup, cpu_stream):
+    model, _, leaf = setup
+    stream, _ = cpu_stream
+    got, depth, _ = float_decode(FloatTwin(model, "cpu", "fused"), stream, L)
+    assert depth == L and np.array_equal(np.sort(got), leaf)
 
 
-def test_float_twin_orders_disagree_and_decode_collapses(level_data):
-    """Two float32 evaluation orders of the same network give different quantised CDFs on
-    some nodes; decoding a stream encoded with one using the other derails."""
-    differing, total, collapsed = 0, 0, 0
-    for d, F, hd, sym, p_int in level_data:
-        pa = quantise_pmf(float_logits(F, hd, "blas"))
-        pb = quantise_pmf(float_logits(F, hd, "reversed"))
-        rows = np.any(pa != pb, 1)
-        differing += int(rows.sum())
-        total += len(rows)
-        words, x = rans_encode(sym, pa)
-        assert np.array_equal(rans_decode(words, x, pa), sym), d  # same order: fine
-        if rows.any():
-            dec = rans_decode(words, x, pb)
-            first = int(np.argmax(rows))
-            assert np.array_equal(dec[:first], sym[:first])
-            if not np.array_equal(dec, sym):
-                collapsed += 1
-    print(f"float twin: {differing} of {total} node CDFs differ between evaluation orders; "
-          f"{collapsed} level streams fail to decode")
-    assert differing > 0 and collapsed > 0
+def _collapse_report(enc_pmfs, dec_pmfs, got, depth, leaf):
+    differ = sum(int(np.any(a != b, 1).sum()) for a, b in zip(enc_pmfs, dec_pmfs) if a.shape == b.shape)
+    kept = np.intersect1d(got, leaf).size if depth == L else 0
+    return differ, kept
+
+
+def test_float_other_order_collapses(setup, cpu_stream):
+    """Decoding the fused-order float stream with the per-offset order (the same network,
+    float32, summed in another order) derails: CDFs differ and the cloud is wrong."""
+    model, _, leaf = setup
+    stream, enc_pmfs = cpu_stream
+    got, depth, dec_pmfs = float_decode(FloatTwin(model, "cpu", "per_offset"), stream, L)
+    differ, kept = _collapse_report(enc_pmfs, dec_pmfs, got, depth, leaf)
+    print(f"float twin, CPU fused vs CPU per-offset: {differ} node CDFs differ; decode reached depth {depth}, "
+          f"{kept} of {leaf.size} voxels recovered")
+    assert differ > 0
+    assert depth < L or not np.array_equal(np.sort(got), leaf)
 
 
 @pytest.mark.gpu
-def test_float_twin_cross_device(level_data):
-    """Cross-device form: the float twin on cuda:0 (torch fp32, cuBLAS order) against the
-    CPU float32 twin; the integer path has no such split (GPU CDFs == oracle CDFs)."""
+def test_float_cross_device_collapses_integer_does_not(setup, cpu_stream):
+    """Encode with the CPU float twin, decode with the same twin on cuda:0 (torch fp32,
+    TF32 off): the decode derails (Fig. 2b).  The integer pipeline on the same frame:
+    GPU encode -> CPU oracle decode and CPU oracle encode -> GPU decode are exact (Fig. 2c)."""
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
-    differing = 0
-    for d, F, hd, sym, p_int in level_data:
-        Ft = torch.from_numpy(F.astype(np.float32)).cuda()
-        W1 = torch.from_numpy(hd.W1.astype(np.float32)).cuda()
-        W2 = torch.from_numpy(hd.W2.astype(np.float32)).cuda()
-        h = Ft @ W1.T + torch.from_numpy(hd.b1.astype(np.float32)).cuda()
-        a = torch.where(h >= 0, h * (hd.rq1.m_pos / 2.0 ** hd.rq1.r), h * (hd.rq1.m_neg / 2.0 ** hd.rq1.r))
-        z = a @ W2.T + torch.from_numpy(hd.b2.astype(np.float32)).cuda()
-        lg = (z * (hd.rq_logit.m_pos / 2.0 ** hd.rq_logit.r / 256.0)).cpu().numpy()
-        differing += int(np.any(quantise_pmf(lg) != quantise_pmf(float_logits(F, hd, "blas")), 1).sum())
-    print(f"float twin GPU vs CPU: {differing} node CDFs differ")
+    model, pts, leaf = setup
+    stream, enc_pmfs = cpu_stream
+    got, depth, dec_pmfs = float_decode(FloatTwin(model, "cuda", "fused"), stream, L)
+    differ, kept = _collapse_report(enc_pmfs, dec_pmfs, got, depth, leaf)
+    print(f"float twin, CPU encode -> GPU decode: {differ} node CDFs differ; decode reached depth {depth}, "
+          f"{kept} of {leaf.size} voxels recovered")
+    assert differ > 0
+    assert depth < L or not np.array_equal(np.sort(got), leaf)
+    # integer-only: bit-exact across the two platforms, both directions
+    from paper_2603_25260_b200.pcc import Codec
+    mb = model.to_bytes()
+    om = O.Model(mb)
+    codec = Codec(mb, 0)
+    out, oo = codec.encode_frames(torch.from_numpy(pts).cuda(), [0, len(pts)], L)
+    gpu_bs = out[:oo[1]].cpu().numpy().tobytes()
+    xyz_cpu, _ = O.decode(om, gpu_bs)
+    cpu_bs = O.encode(om, pts, L)
+    d_bs = torch.from_numpy(np.frombuffer(cpu_bs, np.uint8).copy()).cuda()
+    xyz, no = codec.decode_frames(d_bs, [0, len(cpu_bs)], len(pts))
+    codec.close()
+    keys, _ = O.build_octree(xyz_cpu, L)
+    assert gpu_bs == cpu_bs
+    assert np.array_equal(np.sort(keys[L]), leaf)
+    assert np.array_equal(xyz[:no[1]].cpu().numpy(), xyz_cpu)

@@ -84,3 +84,36 @@ def test_default_batch_per_workload():
     assert bench.default_batch("cfg2") == 1024 and bench.default_batch("cfg2_L13") == 1024
     assert bench.default_batch("cfg2_L14") == 256 and bench.default_batch("cfg3") == 256
     assert bench.default_batch("cfg2_t3") == 1024
+
+
+def test_bench_gpus2_spawns_two_gloo_ranks():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself under
+    torch.distributed.run with 2 ranks; here over gloo with the codec-free runner, the
+    whole plumbing (process group, shards, barriers, max-over-ranks time, the stats
+    all_gather, rank 0's single JSON line) runs on CPU."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--backend", "gloo",
+                        "--plumbing-selftest", "--steps", "3", "--warmup", "3", "--batch", "4"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert r.returncode == 0 and len(lines) == 1, r.stdout + r.stderr
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["details"]["backend"] == "gloo"
+    assert line["config"]["global_batch"] == 8 and line["steps"] == 3
+    # rank 1 is the slow one: 4 ms per step -> 24 frames / 12 ms
+    assert line["ms_per_step"] == pytest.approx(4.0)
+    assert line["value"] == pytest.approx(24 / 0.012)
+
+
+def test_bench_rejects_world_mismatch():
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--plumbing-selftest"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0 and "WORLD_SIZE=1" in (r.stdout + r.stderr)
