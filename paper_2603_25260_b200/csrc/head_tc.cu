@@ -12,10 +12,10 @@
 //      exponentials and the quarter sums of e; the normalisation is reading Q21's
 //      cumulative floors C_i = i + floor(E_i * 65281 / S) (E_i = prefix sum of e):
 //      the encoder needs only C_sym and C_{sym+1} (prefix mass before the true symbol
-//      from pass 2, two exact divisions per node), the decoder writes the whole row
-//      C_0..C_254 (pass 3: e back from TMEM, one exact division per entry: 32-bit
-//      reciprocal estimate + a sign-bit remainder test), staged in smem and copied out
-//      as whole 512-byte rows.
+//      from pass 2, two exact divisions per node); the decoder writes a 112-byte row per
+//      node (pcc_internal.cuh DROW_*: S, 65281 * 2^32 / S, the maximum logit mu, the 15
+//      block prefix masses E_{16k} and the hidden activations a), staged in smem and
+//      copied out whole: the rANS decoder recomputes the 16 logits of the block it needs.
 // Bit-exact with the oracle's cdf_quantize / head_logits (integer arithmetic only).
 #include "pcc_internal.cuh"
 #include "rq.cuh"
@@ -79,11 +79,9 @@ template <int MODE>
 struct SmemLayout {
   static constexpr int B = 0;           // W2 operand 256 x 32 (8 KB)
   static constexpr int A = 8192;        // a operand 128 x 32 (4 KB)
-  // encoder: exp table indexed by delta itself, LUT4[j] = LUT[j >> 2] for j < 4096,
-  // LUT4[4096] = 0; decoder: the compact table LUT[j >> 2] (1024 + the 0 sentinel), since
-  // it stores j = min(delta, 4096) >> 2 in its rows anyway and needs the smem for them
+  // exp table indexed by delta itself, LUT4[j] = LUT[j >> 2] for j < 4096, LUT4[4096] = 0
   static constexpr int LUT = 12288;
-  static constexpr int LUT_N = MODE == 0 ? 4097 : 1025;
+  static constexpr int LUT_N = 4097;
   static constexpr int B2 = LUT + ((LUT_N * 4 + 15) & ~15);  // 1 KB
   static constexpr int W1 = B2 + 1024;           // <= 1 KB
   static constexpr int B1 = W1 + 1024;           // <= 256 B
@@ -91,7 +89,7 @@ struct SmemLayout {
   static constexpr int THOLD = MBAR + 8;
   static constexpr int RED = MBAR + 16;          // [4][128] x (a, b) int32 = 4 KB
   static constexpr int ROWI = RED + 4096;        // [128] x 8 int32 = 4 KB
-  static constexpr int STAGE = ROWI + 4096;      // decoder: 128 rows x DROW_BYTES (74 KB)
+  static constexpr int STAGE = ROWI + 4096;      // decoder: 128 rows x DROW_BYTES (14 KB)
   static constexpr int FST = STAGE + (MODE == 1 ? TILE * DROW_BYTES : 0);  // the tile's F rows (cp.async, <= 8 KB)
   static constexpr int END = FST + TILE * 64;
 };
@@ -132,13 +130,10 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     *reinterpret_cast<uint32_t*>(sB + tc::kmaj_off(rr, 4 * w)) = v;
   }
   for (int k = tid; k < 1024; k += NT) reinterpret_cast<uint32_t*>(sA)[k] = 0u;  // K padding stays 0
-  if constexpr (MODE == 0) {
-    for (int k = tid; k < 4096; k += NT) sLut[k] = lut[k >> 2];
-    if (tid == 0) sLut[4096] = 0u;  // delta >= 4096 (16 nats): e = 0 (reading Q20)
-  } else {
-    for (int k = tid; k < 1024; k += NT) sLut[k] = lut[k];
-    if (tid == 0) sLut[1024] = 0u;
-  }
+  for (int k = tid; k < 4096; k += NT) sLut[k] = lut[k >> 2];
+  if (tid == 0) sLut[4096] = 0u;  // delta >= 4096 (16 nats): e = 0 (reading Q20)
+  if constexpr (MODE == 1)  // row padding stays 0
+    for (int k = tid; k < TILE * DROW_BYTES / 4; k += NT) reinterpret_cast<uint32_t*>(sm + S::STAGE)[k] = 0u;
   for (int k = tid; k < 256; k += NT) sb2[k] = b2[k];
   for (int k = tid; k < H * CW; k += NT) sW1[k] = reinterpret_cast<const int32_t*>(W1)[k];
   for (int k = tid; k < H; k += NT) sb1[k] = b1[k];
@@ -200,9 +195,18 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       for (int hh = 0; hh < HQ; ++hh) ab[hh >> 2] |= (uint32_t(rq8(hacc[hh], rq1)) & 0xffu) << (8 * (hh & 3));
     }
     uint8_t* dst = sA + tc::kmaj_off(r, q * HQ);
-    if constexpr (HQ == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(ab[0], ab[1]);
-    else if constexpr (HQ == 4) *reinterpret_cast<uint32_t*>(dst) = ab[0];
-    else *reinterpret_cast<uint16_t*>(dst) = uint16_t(ab[0]);
+    // decoder: the hidden activations also go into the node's staged row (DROW_A)
+    uint8_t* dra = sm + S::STAGE + r * DROW_BYTES + DROW_A + q * HQ;
+    if constexpr (HQ == 8) {
+      *reinterpret_cast<uint2*>(dst) = make_uint2(ab[0], ab[1]);
+      if (MODE == 1) *reinterpret_cast<uint2*>(dra) = make_uint2(ab[0], ab[1]);
+    } else if constexpr (HQ == 4) {
+      *reinterpret_cast<uint32_t*>(dst) = ab[0];
+      if (MODE == 1) *reinterpret_cast<uint32_t*>(dra) = ab[0];
+    } else {
+      *reinterpret_cast<uint16_t*>(dst) = uint16_t(ab[0]);
+      if (MODE == 1) *reinterpret_cast<uint16_t*>(dra) = uint16_t(ab[0]);
+    }
     if (a_dbg && vr) {
       int8_t* ad = a_dbg + size_t(rw) * H + q * HQ;
 #pragma unroll
@@ -286,43 +290,12 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
     const int32_t nM = -rql.Sp;
     const int64_t C2 = (int64_t(mu) << 32) + 0x7fffffff;
     uint32_t csum[4];  // decoder: the quarter's chunk sums (prefix mass at 16-symbol blocks)
-    uint8_t* jrow = sm + S::STAGE + r * DROW_BYTES + DROW_HDR + 128 * q;  // decoder: this quarter's j
 #pragma unroll 1
     for (int ch = 0; ch < 4; ++ch) {
       uint32_t v[16];
       tmem_ld16(taddr + ch * 16, v);
       tc::tmem_wait_ld();
-      if (MODE == 1 && fastl) {
-        // decoder row entry j = min(delta, 4096) >> 2 (the model LUT index, 1024: e = 0)
-        uint32_t jw[8];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const uint32_t dl = uint32_t(int32_t((int64_t(int32_t(v[k])) * nM + C2) >> 32));
-          const uint32_t jj = min(dl, 4096u) >> 2;
-          if (k & 1) jw[k >> 1] = __byte_perm(jw[k >> 1], jj, 0x5410);
-          else jw[k >> 1] = jj;
-          v[k] = sLut[jj];
-        }
-        *reinterpret_cast<uint4*>(jrow + 32 * ch) = make_uint4(jw[0], jw[1], jw[2], jw[3]);
-        *reinterpret_cast<uint4*>(jrow + 32 * ch + 16) = make_uint4(jw[4], jw[5], jw[6], jw[7]);
-      } else if (MODE == 1) {
-        uint32_t jw[8];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int32_t zz = int32_t(v[k]);
-          int32_t lv = int32_t((int64_t(zz) * lm + lhalf) >> lr);
-          if (SAT && !nosat) {
-            lv = zz > zsat_hi ? (1 << 24) : lv;
-            lv = zz < zsat_lo ? -(1 << 24) : lv;
-          }
-          const uint32_t jj = min(uint32_t(mu - lv), 4096u) >> 2;
-          if (k & 1) jw[k >> 1] = __byte_perm(jw[k >> 1], jj, 0x5410);
-          else jw[k >> 1] = jj;
-          v[k] = sLut[jj];
-        }
-        *reinterpret_cast<uint4*>(jrow + 32 * ch) = make_uint4(jw[0], jw[1], jw[2], jw[3]);
-        *reinterpret_cast<uint4*>(jrow + 32 * ch + 16) = make_uint4(jw[4], jw[5], jw[6], jw[7]);
-      } else if (fastl) {
+      if (fastl) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const uint32_t dl = uint32_t(int32_t((int64_t(int32_t(v[k])) * nM + C2) >> 32));
@@ -384,26 +357,27 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       }
       HEAD_TRACE(4, tr0);
     } else {
-      // decoder row header: S, inv32 = floor(65281 * 2^32 / S), and the prefix mass
-      // E_{16k} before each 16-symbol block (this quarter's blocks k = 4q + ch); the rANS
-      // decoder rebuilds C_i = i + floor(E_i * 65281 / S) where its search needs it
+      // decoder row header: S, inv32 = floor(65281 * 2^32 / S), mu, and the prefix mass
+      // E_{16k} before each 16-symbol block (word 2 + k; this quarter's blocks k = 4q + ch);
+      // the rANS decoder rebuilds C_i = i + floor(E_i * 65281 / S) where its search needs it
       uint32_t* hdr = reinterpret_cast<uint32_t*>(sm + S::STAGE + r * DROW_BYTES);
       uint32_t E = (q > 0 ? s0 : 0u) + (q > 1 ? s1 : 0u) + (q > 2 ? s2 : 0u);  // mass before this quarter
       if (q == 0) {
         hdr[0] = Ssum;
         hdr[1] = uint32_t((65281ull << 32) / uint64_t(Ssum));
+        hdr[2] = uint32_t(mu);
       } else {
-        hdr[1 + 4 * q] = E;  // block 4q
+        hdr[2 + 4 * q] = E;  // block 4q
       }
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
         E += csum[ch];
-        hdr[2 + 4 * q + ch] = E;  // block 4q + ch + 1
+        hdr[3 + 4 * q + ch] = E;  // block 4q + ch + 1
       }
       HEAD_TRACE(4, tr0);
       bar_rows();
       // coalesced copy-out of the lane group's 32 rows (contiguous in global and in smem):
-      // 32 x 37 16-byte chunks over the group's 128 threads
+      // 32 x 7 16-byte chunks over the group's 128 threads
       const uint32_t rows_here = (n - tile * TILE) < uint32_t(TILE) ? (n - tile * TILE) : uint32_t(TILE);
       const uint32_t g0 = 32u * uint32_t(warp & 3);
       const uint32_t grow = rows_here > g0 ? min(32u, rows_here - g0) : 0u;
@@ -413,6 +387,7 @@ __global__ void __launch_bounds__(NT, 2) k_head_tc(const int8_t* __restrict__ F,
       const uint32_t gt = uint32_t(warp >> 2) * 32u + (uint32_t(tid) & 31u);  // 0..127 within the group
 #pragma unroll 2
       for (uint32_t t = gt; t < grow * RCH16; t += 128u) gp[t] = sp[t];
+      (void)csum;
     }
     HEAD_TRACE(5, tr0);
     // next tile: its F rows landed (own copies + row barrier), hidden layer into A and the
@@ -490,7 +465,7 @@ void launch_head(pcc_ctx c, const int8_t* F, uint32_t n, const DHead& L, const u
 void head_cdf_tc(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
                  const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg) {
   if (n == 0) return;
-  Prof p(c, mode == 0 ? "head_enc" : "head_dec", size_t(n) * (C + (mode == 0 ? 1 + 4 : 512)));
+  Prof p(c, mode == 0 ? "head_enc" : "head_dec", size_t(n) * (C + (mode == 0 ? 1 + 4 : DROW_BYTES)));
 #define PCC_HEAD(CC)                                                         \
   if (C == CC && H == CC) {                                                  \
     if (mode == 0 && L.can_saturate) launch_head<CC, CC, 0, true>(c, F, n, L, lut, X, cf, cdf, a_dbg);  \

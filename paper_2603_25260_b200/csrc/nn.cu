@@ -323,17 +323,24 @@ __global__ void __launch_bounds__(256) k_head_cdf(const int8_t* __restrict__ F, 
         E += e[t];
       }
     } else {
-      // decoder row (pcc_internal.cuh DROW_*): S, inv32, E_{16k} (k = 1..15), j entries
+      // decoder row (pcc_internal.cuh DROW_*): S, inv32, mu, E_{16k} (k = 1..15), a
       uint8_t* row = reinterpret_cast<uint8_t*>(cdf) + size_t(node) * DROW_BYTES;
       uint32_t* hdr = reinterpret_cast<uint32_t*>(row);
       if (lane == 0) {
         hdr[0] = s;
         hdr[1] = uint32_t((65281ull << 32) / uint64_t(s));
+        hdr[2] = uint32_t(lmax);
+        hdr[18] = hdr[19] = 0u;
       } else if ((lane & 1) == 0) {
-        hdr[1 + lane / 2] = E;  // mass before symbol 8 lane = 16 (lane / 2)
+        hdr[2 + lane / 2] = E;  // mass before symbol 8 lane = 16 (lane / 2)
       }
-      *reinterpret_cast<uint4*>(row + DROW_HDR + 16 * lane) =
-          make_uint4(jv[0] | jv[1] << 16, jv[2] | jv[3] << 16, jv[4] | jv[5] << 16, jv[6] | jv[7] << 16);
+      if (lane < 8) {
+        uint32_t av = 0u;
+#pragma unroll
+        for (int w = 0; w < HW; ++w) av = (w == lane) ? uint32_t(aw[w]) : av;
+        reinterpret_cast<uint32_t*>(row + DROW_A)[lane] = av;
+      }
+      (void)jv;
     }
   }
 }
@@ -423,7 +430,7 @@ template <int C, int H>
 static void head_ch(pcc_ctx c, const int8_t* F, uint32_t n, const DHead& L, const uint32_t* lut, int mode,
                     const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg) {
   const unsigned grid = std::max(1u, std::min(cdiv(n, 8), unsigned(c->sm_count) * 8u));
-  Prof p(c, mode == 0 ? "head_enc" : "head_dec", size_t(n) * (C + (mode == 0 ? 1 + 4 : 512)));
+  Prof p(c, mode == 0 ? "head_enc" : "head_dec", size_t(n) * (C + (mode == 0 ? 1 + 4 : DROW_BYTES)));
   if (mode == 0)
     k_head_cdf<C, H, 0><<<grid, 256, 0, c->stream>>>(F, n, L.W1, L.b1, L.rq1, L.W2, L.b2, L.rql, lut, X, cf, cdf, a_dbg);
   else

@@ -256,14 +256,16 @@ struct DecSeg {
   uint32_t level_bytes;
   uint32_t last;     // 1 if this is the level's last segment (must end the payload)
 };
-// Decoder row per node (DESIGN.md §5 "decoder rows", reading Q21): u32 S, u32 inv32 =
-// floor(65281 * 2^32 / S), u32 E_{16k} for k = 1..15 (prefix mass before symbol 16k),
-// 3 u32 pad, then u16 j_i = min(delta_i, 4096) >> 2 for i = 0..254 (1024: e = 0) and one
-// pad entry: 592 bytes (16-byte multiple).  The rANS decoder rebuilds
-// C_i = i + floor(E_i * 65281 / S) only where its search needs it.
-constexpr int DROW_BYTES = 592, DROW_HDR = 80, DROW_U16 = DROW_BYTES / 2;
-void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* cdf,
-                 const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes, size_t nsym);
+// Decoder row per node (DESIGN.md §5 "decoder rows", reading Q21): u32 S = sum_i e_i,
+// u32 inv32 = floor(65281 * 2^32 / S), i32 mu = max_i l_i (the Q8 logit maximum), u32
+// E_{16k} for k = 1..15 (prefix mass before symbol 16k) at word 2 + k, 8 zero bytes, then
+// the H hidden activations a (int8, Eq.7's C -> H layer) at byte DROW_A = 80, zero padded
+// to 32 bytes: 112 bytes (a 16-byte multiple for TMA, a 16-byte aligned).  The rANS decoder recomputes the 16 logits of the one block
+// its coarse test selects (z_i = b2_i + a . W2_i, exact int32), their exponentials e_i =
+// LUT[(mu - l_i) >> 2] and C_i = i + floor(E_i * 65281 / S) where its search needs them.
+constexpr int DROW_BYTES = 112, DROW_A = 80, DROW_U16 = DROW_BYTES / 2;
+void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* rows, int H,
+                 const DHead& head, const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes, size_t nsym);
 
 // ---- modelgen.cu ----
 bool model_config_valid(const pcc_model_config& c);

@@ -952,8 +952,8 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
     DecSeg* d_segs = upload(c, "dsegs", segs);
     int kmax = 1;
     for (const DecSeg& sg : segs) kmax = std::max(kmax, lanes_for(sg.n));
-    rans_decode(c, d_segs, int(segs.size()), d_bs, cdf, m->lut, static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d],
-                err, kmax, nd);
+    rans_decode(c, d_segs, int(segs.size()), d_bs, cdf, m->H, net.head_of(d), m->lut,
+                static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d], err, kmax, nd);
     PCC_CUDA(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s));
     PCC_CUDA(cudaStreamSynchronize(s));
     if (herr) throw Error{PCC_ERR_CORRUPT};

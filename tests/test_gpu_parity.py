@@ -183,23 +183,36 @@ def test_encoder_per_tensor_parity(pcc, ctx, C, cfg):
     assert got[0] == want
 
 
-def check_decoder_rows(pcc, ctx, D, d):
-    """The decoder rows of level d (DESIGN.md §5 "Data layout") rebuild exactly the
-    oracle's cumulative bounds C_i = i + floor(E_i 65281 / S) (reading Q21), and the
-    decoded codes are the oracle's."""
+def check_decoder_rows(pcc, ctx, D, d, model, L=12):
+    """The decoder rows of level d (pcc_internal.cuh DROW_*: S, floor(65281 2^32 / S), mu,
+    E_{16k}, a) hold exactly the oracle's hidden activations (a/d), and rebuild exactly
+    the oracle's cumulative bounds C_i = i + floor(E_i 65281 / S) (reading Q21) from the
+    Eq.7 logits z = b2 + a W2 and the Eq.15 exponentials; the decoded codes are the
+    oracle's."""
+    Dd = L - 1 - model.n_deep
+    hd = model.shallow[d].head if d <= Dd else model.deep[d - Dd - 1].head
+    H = model.H
     p = D.get(f"p/{d}", np.uint16).reshape(-1, 255).astype(np.int64)
     cum = np.concatenate([np.zeros((p.shape[0], 1), np.int64), np.cumsum(p, 1)[:, :254]], 1)
-    raw = pcc.pcc_debug_tensor(ctx, f"cdf/{d}")
-    hdr = np.frombuffer(raw, np.uint32).reshape(-1, 148)[:, :20].astype(np.int64)
-    j = np.frombuffer(raw, np.uint16).reshape(-1, 296)[:, 40:40 + 255].astype(np.int64)
-    # decoder row: S, floor(65281 2^32 / S), E_{16k}, then the LUT index of every symbol
-    lut = np.concatenate([I.exp_lut().astype(np.int64), [0]])
-    e = lut[j]
+    raw = np.frombuffer(pcc.pcc_debug_tensor(ctx, f"cdf/{d}"), np.uint8).reshape(-1, 112)
+    hdr = raw[:, :72].copy().view(np.uint32).astype(np.int64)
+    a = raw[:, 80:80 + H].copy().view(np.int8).astype(np.int64)
+    assert np.array_equal(a, D.get(f"a/{d}", np.int8).reshape(-1, H).astype(np.int64)), d
+    assert not raw[:, 72:80].any() and not raw[:, 80 + H:].any(), d
+    z = a @ hd.W2.astype(np.int64).T + hd.b2.astype(np.int64)
+    assert np.array_equal(z, D.get(f"z/{d}", np.int32).reshape(-1, 255).astype(np.int64)), d
+    m_l, r_l = hd.rq_logit.m_pos, hd.rq_logit.r
+    l = np.clip((z * m_l + ((1 << (r_l - 1)) if r_l else 0)) >> r_l, -(1 << 24), 1 << 24)
+    mu = l.max(1)
+    assert np.array_equal(hdr[:, 2].astype(np.uint32).view(np.int32).astype(np.int64), mu), d
+    dl = mu[:, None] - l
+    lut = I.exp_lut().astype(np.int64)
+    e = np.where(dl < 4096, lut[np.minimum(dl, 4095) >> 2], 0)
     E = np.concatenate([np.zeros((e.shape[0], 1), np.int64), np.cumsum(e, 1)], 1)
     S = hdr[:, 0]
     assert np.array_equal(E[:, 255], S), d
     assert np.array_equal(hdr[:, 1], (65281 << 32) // S), d
-    assert np.array_equal(hdr[:, 2:17], E[:, 16:241:16]), d
+    assert np.array_equal(hdr[:, 3:18], E[:, 16:241:16]), d
     C = np.arange(255)[None, :] + (E[:, :255] * 65281) // S[:, None]
     assert np.array_equal(C, cum), d
     assert np.array_equal(np.frombuffer(pcc.pcc_debug_tensor(ctx, f"code/{d}"), np.uint8),
@@ -215,8 +228,9 @@ def test_decoder_cdf_parity(pcc, ctx):
     pcc.pcc_ctx_set_debug(ctx, True)
     try:
         out = gpu_decode(pcc, ctx, m, [bs], len(pts))
+        mobj = I.make_model(C=8, H=8, seed=1, min_depth=9, max_depth=18)
         for d in range(4, 12):
-            check_decoder_rows(pcc, ctx, D, d)
+            check_decoder_rows(pcc, ctx, D, d, mobj)
     finally:
         pcc.pcc_ctx_set_debug(ctx, False)
     assert np.array_equal(out[0], morton_sorted_unique(pts, 12))

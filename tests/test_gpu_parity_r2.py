@@ -148,25 +148,35 @@ def test_raw_freq_large_prefix(pcc, ctx):
 # Eq.15 clamp: a logit requant that saturates at +-2^24 (SAT=true predictor kernels)
 # ---------------------------------------------------------------------------------------
 
-@pytest.mark.parametrize("m_l", [783, 3054])
+@pytest.mark.parametrize("sat_frac", [0.02, 0.4])
 @pytest.mark.parametrize("C", [8, 32])
-def test_saturating_logit_requant(pcc, ctx, m_l, C):
+def test_saturating_logit_requant(pcc, ctx, sat_frac, C):
+    """m_l / 2^r_l set so that a fraction sat_frac of the logits clamp at +-2^24 (Eq.15,
+    reading Q20); z itself does not depend on the logit requant, so m_l is derived from
+    the unclamped model's z dumps."""
     model = I.make_model(C=C, H=C, seed=5, min_depth=9, max_depth=14)
+    pts = I.make_frame(I.CFG1, 3)
+    D0 = O.Dump()
+    O.encode(O.Model(model.to_bytes()), pts, 12, D0)
+    z = np.concatenate([D0.get(f"z/{d}", np.int32) for d in range(4, 12)]).astype(np.int64)
+    m_l = int(np.ceil((1 << 24) / np.quantile(np.abs(z), 1.0 - sat_frac)))
     for h in [s.head for s in model.shallow.values()] + [dp.head for dp in model.deep]:
         h.rq_logit = I.RQ(m_l, m_l, 0)
     mb = model.to_bytes()
     om = O.Model(mb)
-    pts = I.make_frame(I.CFG1, 3)
     D = O.Dump()
     O.encode(om, pts, 12, D)
-    z = np.concatenate([D.get(f"z/{d}", np.int32) for d in range(4, 12)]).astype(np.int64)
-    assert (np.abs(z * m_l) >= 1 << 24).mean() > 0.005   # the clamp is exercised
+    frac = (np.abs(z * m_l) >= 1 << 24).mean()
+    assert 0.5 * sat_frac < frac < 2 * sat_frac   # the clamp is exercised
     m = pcc.pcc_model_load(mb, 0)
     try:
         pcc.pcc_ctx_set_debug(ctx, True)
         try:
             gpu_encode(pcc, ctx, m, [pts], 12)
             assert _compare_dumps(pcc, ctx, D, 12) > 30
+            gpu_decode(pcc, ctx, m, [O.encode(om, pts, 12)], len(pts))
+            for d in range(4, 12):
+                check_decoder_rows(pcc, ctx, D, d, model)
         finally:
             pcc.pcc_ctx_set_debug(ctx, False)
         _check_frames(pcc, ctx, m, om, [pts, I.make_frame(I.CFG2, 1)], 12)
@@ -179,7 +189,8 @@ def test_saturating_logit_requant(pcc, ctx, m_l, C):
 # ---------------------------------------------------------------------------------------
 
 def test_decoder_rows_c32(pcc, ctx):
-    mb = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18).to_bytes()
+    mobj = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18)
+    mb = mobj.to_bytes()
     om = O.Model(mb)
     m = pcc.pcc_model_load(mb, 0)
     try:
@@ -190,7 +201,7 @@ def test_decoder_rows_c32(pcc, ctx):
         try:
             out = gpu_decode(pcc, ctx, m, [bs], len(pts))
             for d in range(4, 12):
-                check_decoder_rows(pcc, ctx, D, d)
+                check_decoder_rows(pcc, ctx, D, d, mobj)
         finally:
             pcc.pcc_ctx_set_debug(ctx, False)
         assert np.array_equal(out[0], morton_sorted_unique(pts, 12))
