@@ -294,12 +294,14 @@ void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, c
   if (nseg == 0) return;
   const int stage_rows = max_lanes <= 8 ? 8 : (max_lanes <= 16 ? 16 : 32);
   const size_t smem = size_t(DEC_WPC) * 2 * stage_rows * DROW_BYTES;
+  // the attribute is set once per device: to the largest launch (32 rows per stage)
+  constexpr size_t smem_max = size_t(DEC_WPC) * 2 * 32 * DROW_BYTES;
   const unsigned grid = unsigned((nseg + DEC_WPC - 1) / DEC_WPC);
   // algorithmic bytes: the 112-byte row and one 16-bit word per symbol
   Prof p(c, "rans_dec", nsym * (DROW_BYTES + 2));
 #define PCC_DEC(HH, SS)                                                                                         \
   if (H == HH && hd.can_saturate == SS) {                                                                      \
-    PCC_SMEM_ATTR((k_rans_dec<HH, SS>), smem);                                                                 \
+    PCC_SMEM_ATTR((k_rans_dec<HH, SS>), smem_max);                                                             \
     k_rans_dec<HH, SS><<<grid, 32 * DEC_WPC, smem, c->stream>>>(d_segs, nseg, bs,                              \
                                                                 reinterpret_cast<const uint8_t*>(rows), hd.W2, \
                                                                 hd.b2, hd.rql, hd.zsat_lo, hd.zsat_hi, lut, X, \

@@ -43,7 +43,12 @@ void* pinned(pcc_ctx c, size_t bytes) {
   return c->pinned;
 }
 
-void launched(pcc_ctx c, int n) { c->launches += uint64_t(n); }
+// Called after every launch: counts it and surfaces a failed launch (bad configuration,
+// shared-memory limit) immediately instead of as a wrong result later.
+void launched(pcc_ctx c, int n) {
+  c->launches += uint64_t(n);
+  PCC_CUDA(cudaPeekAtLastError());
+}
 
 static cudaEvent_t ev_get(pcc_ctx c) {
   if (!c->pool.empty()) {
