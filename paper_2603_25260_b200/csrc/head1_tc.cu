@@ -1,0 +1,329 @@
+// head1_tc.cu — occupancy predictor (Eq.7) + integer softmax to a Q16 pmf
+// (Eq.15; readings Q20-Q22), one THREAD per node.
+//
+// A CTA is 4 warps = 128 threads = one 128-node tile per iteration (persistent).  Warp w
+// owns TMEM lanes 32w..32w+31, so thread t owns node t of the tile and ALL 256 logit
+// columns of its TMEM lane: the softmax needs no cross-thread exchange and no row
+// barriers (the round-1 kernel split a row over 4 threads in 4 warps and synchronised
+// them 5 times per tile).  Per tile:
+//   1. hidden layer a = prq(W1 F + b1) (C -> H, dp4a) of the thread's node, written into
+//      the tcgen05 A operand (canonical K-major smem tile) and kept in registers;
+//   2. the logit bias b2 is stored into the thread's TMEM lane (tcgen05.st); one
+//      tcgen05.mma.kind::i8 (M = 128, N = 256, K = 32) adds a W2^T onto it: z = b2 + a W2^T;
+//   3. pass 1: max z (and min z when the model can saturate) over 16 chunks of 16 columns
+//      (tcgen05.ld 32x32b.x16); the Q8 logit requant is monotone, so mu = l(max z);
+//   4. pass 2: delta = mu - l(z) (one IMAD.HI in the signed fast form), e = LUT[delta >> 2]
+//      (0 beyond 16 nats), the 16-symbol chunk sums; encoder: the prefix mass before the
+//      true symbol and its e -> (C_sym, freq) by two exact divisions (reading Q21);
+//      decoder: the 112-byte row (S, 65281 * 2^32 / S, mu, E_{16k}, a) stored directly.
+// The exp table is held as 4 interleaved copies of LUT4[delta] = LUT[delta >> 2] (16 bytes
+// per delta, lane l reads copy l & 3): 8 lanes per copy spread over 8 banks by delta mod 8,
+// fewer shared-memory wavefronts per random lookup than one copy.  Two CTAs per SM (256
+// TMEM columns each).  Bit-exact with the oracle's head_logits / cdf_quantize.
+#include "pcc_internal.cuh"
+#include "rq.cuh"
+#include "tc.cuh"
+
+namespace pcc {
+
+namespace {
+
+constexpr int TILE = 128, NT1 = 128;
+constexpr uint32_t IDESC = tc::idesc_i8(128, 256);
+
+__device__ __forceinline__ int32_t lq8(int32_t z, const RQ& q) {  // Q8 logit, clamp +-2^24
+  int64_t v = int64_t(z) * int64_t(q.mp);
+  if (q.r > 0) v = (v + (int64_t(1) << (q.r - 1))) >> q.r;
+  v = v < -(int64_t(1) << 24) ? -(int64_t(1) << 24) : (v > (int64_t(1) << 24) ? (int64_t(1) << 24) : v);
+  return int32_t(v);
+}
+
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+
+struct Smem1 {
+  static constexpr int B = 0;                      // W2 operand 256 x 32 (8 KB)
+  static constexpr int A = 8192;                   // a operand 128 x 32 (4 KB)
+  static constexpr int B2 = 12288;                 // b2 [256] (1 KB)
+  static constexpr int W1 = B2 + 1024;             // W1 words [H][C/4] (<= 1 KB)
+  static constexpr int B1 = W1 + 1024;             // b1 [H] (<= 256 B)
+  static constexpr int MBAR = B1 + 256;
+  static constexpr int THOLD = MBAR + 8;
+  static constexpr int LUT = MBAR + 128;           // [4097][4] u32: copy c of LUT4[delta] at 16 delta + 4c
+  static constexpr int END = LUT + 4097 * 16;
+};
+
+template <int C, int H, int MODE, bool SAT>
+__global__ void __launch_bounds__(NT1, 2) k_head1_tc(const int8_t* __restrict__ F, uint32_t n,
+                                                     const int8_t* __restrict__ W1, const int32_t* __restrict__ b1, RQ rq1,
+                                                     const int8_t* __restrict__ W2, const int32_t* __restrict__ b2, RQ rql,
+                                                     const uint32_t* __restrict__ lut, const uint8_t* __restrict__ X,
+                                                     uint32_t* __restrict__ cf, uint8_t* __restrict__ rows,
+                                                     int8_t* __restrict__ a_dbg, int32_t zsat_lo, int32_t zsat_hi) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  using S = Smem1;
+  constexpr int CW = C / 4, HW = H / 4;
+  uint8_t* sB = sm + S::B;
+  uint8_t* sA = sm + S::A;
+  int32_t* sb2 = reinterpret_cast<int32_t*>(sm + S::B2);
+  int32_t* sW1 = reinterpret_cast<int32_t*>(sm + S::W1);
+  int32_t* sb1 = reinterpret_cast<int32_t*>(sm + S::B1);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + S::MBAR);
+  uint32_t* thold = reinterpret_cast<uint32_t*>(sm + S::THOLD);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  for (int k = tid; k < 256 * 8; k += NT1) {
+    const int rr = k >> 3, w = k & 7;
+    const uint32_t v = (w < HW) ? reinterpret_cast<const uint32_t*>(W2)[rr * HW + w] : 0u;
+    *reinterpret_cast<uint32_t*>(sB + tc::kmaj_off(rr, 4 * w)) = v;
+  }
+  for (int k = tid; k < 1024; k += NT1) reinterpret_cast<uint32_t*>(sA)[k] = 0u;  // K padding stays 0
+  for (int k = tid; k < 4097; k += NT1) {
+    const uint32_t v = k < 4096 ? lut[k >> 2] : 0u;  // delta >= 4096 (16 nats): e = 0 (reading Q20)
+    *reinterpret_cast<uint4*>(sm + S::LUT + 16 * k) = make_uint4(v, v, v, v);
+  }
+  for (int k = tid; k < 256; k += NT1) sb2[k] = b2[k];
+  for (int k = tid; k < H * CW; k += NT1) sW1[k] = reinterpret_cast<const int32_t*>(W1)[k];
+  for (int k = tid; k < H; k += NT1) sb1[k] = b1[k];
+  if (warp == 0) tc::tmem_alloc<256>(thold);
+  if (tid == 0) tc::mbar_init(mbar, 1);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = *thold;
+  const uint32_t taddr = tbase + (uint32_t(32 * warp) << 16);  // this thread's TMEM lane
+  const uint64_t adesc = tc::sdesc(tc::smem_u32(sA));
+  const uint64_t bdesc = tc::sdesc(tc::smem_u32(sB));
+  const uint32_t* lutp = reinterpret_cast<const uint32_t*>(sm + S::LUT) + (lane & 3);  // copy lane & 3
+  const uint32_t ntiles = (n + TILE - 1) / TILE;
+  const int64_t lhalf = rql.r > 0 ? (int64_t(1) << (rql.r - 1)) : 0;
+  uint32_t phase = 0;
+
+  // the thread's node row F (C bytes) of tile tl, as C/4 words
+  auto load_f = [&](uint32_t tl, uint32_t (&fw)[CW]) {
+    const uint32_t rw = tl * TILE + uint32_t(tid);
+    if (tl < ntiles && rw < n) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(F + size_t(rw) * C);
+      if constexpr (CW % 4 == 0) {
+#pragma unroll
+        for (int w = 0; w < CW; w += 4) {
+          const uint4 v = *reinterpret_cast<const uint4*>(src + w);
+          fw[w] = v.x, fw[w + 1] = v.y, fw[w + 2] = v.z, fw[w + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int w = 0; w < CW; ++w) fw[w] = src[w];
+      }
+    } else {
+#pragma unroll
+      for (int w = 0; w < CW; ++w) fw[w] = 0u;
+    }
+  };
+  // hidden layer of the thread's node into the A operand (and aw), then b2 into its TMEM lane
+  auto hidden_and_bias = [&](uint32_t tl, const uint32_t (&fw)[CW], uint32_t (&aw)[HW]) {
+    const uint32_t rw = tl * TILE + uint32_t(tid);
+#pragma unroll
+    for (int g4 = 0; g4 < HW; ++g4) {
+      int32_t hacc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int h = 4 * g4 + u;
+        int32_t acc = sb1[h];
+#pragma unroll
+        for (int w = 0; w < CW; ++w) acc = __dp4a(int32_t(fw[w]), sW1[h * CW + w], acc);
+        hacc[u] = acc;
+      }
+      if (rq1.fast_s)
+        aw[g4] = pack_sat4(rq_s(hacc[0], rq1), rq_s(hacc[1], rq1), rq_s(hacc[2], rq1), rq_s(hacc[3], rq1));
+      else
+        aw[g4] = (uint32_t(rq8(hacc[0], rq1)) & 0xffu) | (uint32_t(rq8(hacc[1], rq1)) & 0xffu) << 8 |
+                 (uint32_t(rq8(hacc[2], rq1)) & 0xffu) << 16 | (uint32_t(rq8(hacc[3], rq1)) & 0xffu) << 24;
+      *reinterpret_cast<uint32_t*>(sA + tc::kmaj_off(uint32_t(tid), 4 * g4)) = aw[g4];
+    }
+    if (a_dbg && rw < n) {
+#pragma unroll
+      for (int g4 = 0; g4 < HW; ++g4) reinterpret_cast<uint32_t*>(a_dbg + size_t(rw) * H)[g4] = aw[g4];
+    }
+#pragma unroll
+    for (int ch = 0; ch < 16; ++ch) {
+      uint32_t bv[16];
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const uint4 b4 = *reinterpret_cast<const uint4*>(sb2 + 16 * ch + 4 * k4);
+        bv[4 * k4] = b4.x, bv[4 * k4 + 1] = b4.y, bv[4 * k4 + 2] = b4.z, bv[4 * k4 + 3] = b4.w;
+      }
+      st16(taddr + ch * 16, bv);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  };
+
+  uint32_t fw[CW], aw[HW];
+  load_f(blockIdx.x, fw);
+  if (blockIdx.x < ntiles) hidden_and_bias(blockIdx.x, fw, aw);
+  load_f(blockIdx.x + gridDim.x, fw);
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t row = tile * TILE + uint32_t(tid);
+    const bool valid = row < n;
+    // A operand (all 128 rows) and the bias-initialised accumulator are complete
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid == 0) {
+      tc::mma_i8(tbase, adesc, bdesc, IDESC, 1u);
+      tc::commit(mbar);
+    }
+    tc::mbar_wait(mbar, phase);
+    phase ^= 1u;
+    tc::fence_after();
+
+    // ---- pass 1: max z (and min z) over the 255 symbols (column 255 is padding) ----
+    int32_t zmx = INT32_MIN, zmn = INT32_MAX;
+#pragma unroll 1
+    for (int ch = 0; ch < 16; ++ch) {
+      uint32_t v[16];
+      ld16(taddr + ch * 16, v);
+      tc::tmem_wait_ld();
+      const bool pad = ch == 15;
+#pragma unroll
+      for (int k = 0; k < 15; ++k) {
+        zmx = max(zmx, int32_t(v[k]));
+        if (SAT) zmn = min(zmn, int32_t(v[k]));
+      }
+      zmx = max(zmx, pad ? INT32_MIN : int32_t(v[15]));
+      if (SAT) zmn = min(zmn, pad ? INT32_MAX : int32_t(v[15]));
+    }
+    const int32_t mu = lq8(zmx, rql);
+    const bool nosat = !SAT || (zmx <= zsat_hi && zmn >= zsat_lo);
+    const bool fastl = rql.fast_s && nosat;
+    const int32_t nM = -rql.Sp;
+    const int64_t C2 = (int64_t(mu) << 32) + 0x7fffffff;
+    const int sym = (MODE == 0 && valid) ? int(X[row]) - 1 : 0;
+
+    // ---- pass 2: e_i = LUT[(mu - l_i) >> 2], chunk sums, the encoder's prefix mass ----
+    uint32_t S = 0, pre = 0, es = 0;
+    uint32_t Eb[16];  // decoder: prefix mass before each 16-symbol block
+#pragma unroll 1
+    for (int ch = 0; ch < 16; ++ch) {
+      uint32_t v[16];
+      ld16(taddr + ch * 16, v);
+      tc::tmem_wait_ld();
+      if (fastl) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const uint32_t dl = uint32_t(int32_t((int64_t(int32_t(v[k])) * nM + C2) >> 32));
+          v[k] = lutp[4u * min(dl, 4096u)];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int32_t zz = int32_t(v[k]);
+          int32_t lv = int32_t((int64_t(zz) * int64_t(rql.mp) + lhalf) >> rql.r);
+          if (SAT && !nosat) {
+            lv = zz > zsat_hi ? (1 << 24) : lv;
+            lv = zz < zsat_lo ? -(1 << 24) : lv;
+          }
+          v[k] = lutp[4u * min(uint32_t(mu - lv), 4096u)];
+        }
+      }
+      if (ch == 15) v[15] = 0u;  // column 255 is padding, not a symbol
+      uint32_t cs = 0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) cs += v[k];
+      if constexpr (MODE == 0) {
+        const int i0 = 16 * ch;
+        if (sym >= i0 + 16) {
+          pre += cs;
+        } else if (sym >= i0) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            pre += (i0 + k < sym) ? v[k] : 0u;
+            es = (i0 + k == sym) ? v[k] : es;
+          }
+        }
+      } else {
+        Eb[ch] = S;
+      }
+      S += cs;  // <= 255 * 2^24 < 2^32
+    }
+    // all of this thread's TMEM reads are done: the next tile may be set up
+    if constexpr (MODE == 0) {
+      if (valid) {  // (cum, freq) = (C_sym, C_{sym+1} - C_sym), reading Q21
+        const uint32_t c0 = uint32_t(sym) + uint32_t((uint64_t(pre) * 65281ull) / S);
+        const uint32_t c1 = uint32_t(sym) + 1u + uint32_t((uint64_t(pre + es) * 65281ull) / S);
+        cf[row] = c0 | ((c1 - c0) << 16);
+      }
+    } else if (valid) {
+      // decoder row (pcc_internal.cuh DROW_*): S, inv32, mu, E_{16k} k = 1..15, 0, 0, a
+      uint4* dst = reinterpret_cast<uint4*>(rows + size_t(row) * DROW_BYTES);
+      const uint32_t inv32 = uint32_t((65281ull << 32) / uint64_t(S));
+      dst[0] = make_uint4(S, inv32, uint32_t(mu), Eb[1]);
+      dst[1] = make_uint4(Eb[2], Eb[3], Eb[4], Eb[5]);
+      dst[2] = make_uint4(Eb[6], Eb[7], Eb[8], Eb[9]);
+      dst[3] = make_uint4(Eb[10], Eb[11], Eb[12], Eb[13]);
+      dst[4] = make_uint4(Eb[14], Eb[15], 0u, 0u);
+      uint32_t ap[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) ap[w] = w < HW ? aw[w < HW ? w : 0] : 0u;
+      dst[5] = make_uint4(ap[0], ap[1], ap[2], ap[3]);
+      dst[6] = make_uint4(ap[4], ap[5], ap[6], ap[7]);
+    }
+    // next tile: hidden layer into A (this tile's MMA has completed) and b2 into TMEM
+    if (tile + gridDim.x < ntiles) {
+      hidden_and_bias(tile + gridDim.x, fw, aw);
+      load_f(tile + 2 * gridDim.x, fw);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<256>(tbase);
+}
+
+template <int C, int H, int MODE, bool SAT>
+void launch_head1(pcc_ctx c, const int8_t* F, uint32_t n, const DHead& L, const uint32_t* lut, const uint8_t* X,
+                  uint32_t* cf, uint16_t* rows, int8_t* a_dbg) {
+  auto kern = k_head1_tc<C, H, MODE, SAT>;
+  PCC_SMEM_ATTR(kern, Smem1::END);
+  const uint32_t ntiles = (n + TILE - 1) / TILE;
+  const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 2u));
+  kern<<<grid, NT1, Smem1::END, c->stream>>>(F, n, L.W1, L.b1, L.rq1, L.W2, L.b2, L.rql, lut, X, cf,
+                                            reinterpret_cast<uint8_t*>(rows), a_dbg, L.zsat_lo, L.zsat_hi);
+  launched(c);
+}
+
+}  // namespace
+
+void head_cdf_tc1(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
+                  const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg) {
+  if (n == 0) return;
+  Prof p(c, mode == 0 ? "head_enc" : "head_dec", size_t(n) * (C + (mode == 0 ? 1 + 4 : DROW_BYTES)));
+#define PCC_HEAD1(CC)                                                                                    \
+  if (C == CC && H == CC) {                                                                              \
+    if (mode == 0 && L.can_saturate) launch_head1<CC, CC, 0, true>(c, F, n, L, lut, X, cf, cdf, a_dbg);  \
+    else if (mode == 0) launch_head1<CC, CC, 0, false>(c, F, n, L, lut, X, cf, cdf, a_dbg);              \
+    else if (L.can_saturate) launch_head1<CC, CC, 1, true>(c, F, n, L, lut, X, cf, cdf, a_dbg);          \
+    else launch_head1<CC, CC, 1, false>(c, F, n, L, lut, X, cf, cdf, a_dbg);                             \
+    return;                                                                                              \
+  }
+  PCC_HEAD1(8)
+  PCC_HEAD1(16)
+  PCC_HEAD1(32)
+#undef PCC_HEAD1
+  throw Error{PCC_ERR_INVALID_ARG};
+}
+
+}  // namespace pcc

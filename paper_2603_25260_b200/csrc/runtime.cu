@@ -106,16 +106,20 @@ namespace {
 
 inline unsigned cdiv(size_t a, size_t b) { return unsigned((a + b - 1) / b); }
 
-// Predictor + softmax: tcgen05 path by default; PCC_HEAD=simt selects the dp4a
-// warp-per-node kernel (kept as the A/B baseline; both are bit-exact).
+// Predictor + softmax: the one-thread-per-node tcgen05 kernel (head1_tc.cu) by default;
+// PCC_HEAD=q4 selects the round-1 tcgen05 kernel (4 threads per node), PCC_HEAD=simt the
+// dp4a warp-per-node kernel (A/B baselines; all are bit-exact).
 void head_any(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
               const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg) {
-  static const bool simt = [] {
+  static const int which = [] {
     const char* e = getenv("PCC_HEAD");
-    return e && std::string(e) == "simt";
+    if (e && std::string(e) == "simt") return 2;
+    if (e && std::string(e) == "q4") return 1;
+    return 0;
   }();
-  if (simt) head_cdf(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
-  else head_cdf_tc(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
+  if (which == 2) head_cdf(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
+  else if (which == 1) head_cdf_tc(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
+  else head_cdf_tc1(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
 }
 
 inline int lanes_for(uint32_t n) {
