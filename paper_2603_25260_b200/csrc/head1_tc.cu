@@ -1,8 +1,8 @@
 // head1_tc.cu — occupancy predictor (Eq.7) + integer softmax to a Q16 pmf
 // (Eq.15; readings Q20-Q22), one THREAD per node.
 //
-// A CTA is 4 warps = 128 threads = one 128-node tile per iteration (persistent).  Warp w
-// owns TMEM lanes 32w..32w+31, so thread t owns node t of the tile and ALL 256 logit
+// A tile group is 4 warps = 128 threads = one 128-node tile per iteration (persistent).
+// Warp w owns TMEM lanes 32(w%4)..+31, so thread t owns node t of the tile and ALL 256 logit
 // columns of its TMEM lane: the softmax needs no cross-thread exchange and no row
 // barriers (the round-1 kernel split a row over 4 threads in 4 warps and synchronised
 // them 5 times per tile).  Per tile:
@@ -10,16 +10,15 @@
 //      the tcgen05 A operand (canonical K-major smem tile) and kept in registers;
 //   2. the logit bias b2 is stored into the thread's TMEM lane (tcgen05.st); one
 //      tcgen05.mma.kind::i8 (M = 128, N = 256, K = 32) adds a W2^T onto it: z = b2 + a W2^T;
-//   3. pass 1: max z (and min z when the model can saturate) over 16 chunks of 16 columns
-//      (tcgen05.ld 32x32b.x16); the Q8 logit requant is monotone, so mu = l(max z);
+//   3. pass 1: max z (and min z when the model can saturate) over 8 chunks of 32 columns
+//      (tcgen05.ld 32x32b.x32); the Q8 logit requant is monotone, so mu = l(max z);
 //   4. pass 2: delta = mu - l(z) (one IMAD.HI in the signed fast form), e = LUT[delta >> 2]
 //      (0 beyond 16 nats), the 16-symbol chunk sums; encoder: the prefix mass before the
 //      true symbol and its e -> (C_sym, freq) by two exact divisions (reading Q21);
 //      decoder: the 112-byte row (S, 65281 * 2^32 / S, mu, E_{16k}, a) stored directly.
-// The exp table is held as 4 interleaved copies of LUT4[delta] = LUT[delta >> 2] (16 bytes
-// per delta, lane l reads copy l & 3): 8 lanes per copy spread over 8 banks by delta mod 8,
-// fewer shared-memory wavefronts per random lookup than one copy.  Two CTAs per SM (256
-// TMEM columns each).  Bit-exact with the oracle's head_logits / cdf_quantize.
+// One CTA per SM runs two such tile pipelines (2 x 256 TMEM columns) that share a 32-copy
+// interleaved exp table (conflict-free random lookups).  Bit-exact with the oracle's
+// head_logits / cdf_quantize.
 #include "pcc_internal.cuh"
 #include "rq.cuh"
 #include "tc.cuh"
@@ -28,7 +27,7 @@ namespace pcc {
 
 namespace {
 
-constexpr int TILE = 128, NT1 = 128;
+constexpr int TILE = 128, NT1 = 256;
 constexpr uint32_t IDESC = tc::idesc_i8(128, 256);
 
 __device__ __forceinline__ int32_t lq8(int32_t z, const RQ& q) {  // Q8 logit, clamp +-2^24
@@ -38,14 +37,6 @@ __device__ __forceinline__ int32_t lq8(int32_t z, const RQ& q) {  // Q8 logit, c
   return int32_t(v);
 }
 
-__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-}
 __device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -54,20 +45,26 @@ __device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&v)[16]) {
       "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
 }
 
+// One CTA per SM: 8 warps = 2 tile groups of 4 warps, each group an independent 128-node
+// tile pipeline with its own A operand, 256 TMEM columns (512 per SM), mbarrier and named
+// barrier; they share the W2 operand, b2 / W1 / b1 and the exp table.  The table is held
+// as 32 interleaved copies of the compact LUT (1025 entries, LUT[1024] = 0): lane l reads
+// copy l, word 32 idx + l, so a warp's 32 random lookups hit 32 distinct banks (one
+// shared-memory wavefront each).
 struct Smem1 {
   static constexpr int B = 0;                      // W2 operand 256 x 32 (8 KB)
-  static constexpr int A = 8192;                   // a operand 128 x 32 (4 KB)
-  static constexpr int B2 = 12288;                 // b2 [256] (1 KB)
+  static constexpr int A = 8192;                   // a operands, one 128 x 32 tile per group (2 x 4 KB)
+  static constexpr int B2 = A + 8192;              // b2 [256] (1 KB)
   static constexpr int W1 = B2 + 1024;             // W1 words [H][C/4] (<= 1 KB)
   static constexpr int B1 = W1 + 1024;             // b1 [H] (<= 256 B)
-  static constexpr int MBAR = B1 + 256;
-  static constexpr int THOLD = MBAR + 8;
-  static constexpr int LUT = MBAR + 128;           // [4097][4] u32: copy c of LUT4[delta] at 16 delta + 4c
-  static constexpr int END = LUT + 4097 * 16;
+  static constexpr int MBAR = B1 + 256;            // 2 mbarriers
+  static constexpr int THOLD = MBAR + 16;
+  static constexpr int LUT = MBAR + 128;           // [1025][32] u32
+  static constexpr int END = LUT + 1025 * 32 * 4;
 };
 
 template <int C, int H, int MODE, bool SAT>
-__global__ void __launch_bounds__(NT1, 2) k_head1_tc(const int8_t* __restrict__ F, uint32_t n,
+__global__ void __launch_bounds__(NT1, 1) k_head1_tc(const int8_t* __restrict__ F, uint32_t n,
                                                      const int8_t* __restrict__ W1, const int32_t* __restrict__ b1, RQ rq1,
                                                      const int8_t* __restrict__ W2, const int32_t* __restrict__ b2, RQ rql,
                                                      const uint32_t* __restrict__ lut, const uint8_t* __restrict__ X,
@@ -76,46 +73,50 @@ __global__ void __launch_bounds__(NT1, 2) k_head1_tc(const int8_t* __restrict__ 
   extern __shared__ __align__(1024) uint8_t sm[];
   using S = Smem1;
   constexpr int CW = C / 4, HW = H / 4;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tg = warp >> 2;          // tile group
+  const int r = tid & (TILE - 1);    // node of the group's tile = TMEM lane
   uint8_t* sB = sm + S::B;
-  uint8_t* sA = sm + S::A;
+  uint8_t* sA = sm + S::A + 4096 * tg;
   int32_t* sb2 = reinterpret_cast<int32_t*>(sm + S::B2);
   int32_t* sW1 = reinterpret_cast<int32_t*>(sm + S::W1);
   int32_t* sb1 = reinterpret_cast<int32_t*>(sm + S::B1);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + S::MBAR);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + S::MBAR) + tg;
   uint32_t* thold = reinterpret_cast<uint32_t*>(sm + S::THOLD);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   for (int k = tid; k < 256 * 8; k += NT1) {
     const int rr = k >> 3, w = k & 7;
     const uint32_t v = (w < HW) ? reinterpret_cast<const uint32_t*>(W2)[rr * HW + w] : 0u;
     *reinterpret_cast<uint32_t*>(sB + tc::kmaj_off(rr, 4 * w)) = v;
   }
-  for (int k = tid; k < 1024; k += NT1) reinterpret_cast<uint32_t*>(sA)[k] = 0u;  // K padding stays 0
-  for (int k = tid; k < 4097; k += NT1) {
-    const uint32_t v = k < 4096 ? lut[k >> 2] : 0u;  // delta >= 4096 (16 nats): e = 0 (reading Q20)
-    *reinterpret_cast<uint4*>(sm + S::LUT + 16 * k) = make_uint4(v, v, v, v);
+  for (int k = tid; k < 2048; k += NT1) reinterpret_cast<uint32_t*>(sm + S::A)[k] = 0u;  // K padding stays 0
+  for (int k = tid; k < 1025 * 32; k += NT1) {
+    const int idx = k >> 5;  // delta >= 4096 (16 nats): index 1024, e = 0 (reading Q20)
+    reinterpret_cast<uint32_t*>(sm + S::LUT)[k] = idx < 1024 ? lut[idx] : 0u;
   }
   for (int k = tid; k < 256; k += NT1) sb2[k] = b2[k];
   for (int k = tid; k < H * CW; k += NT1) sW1[k] = reinterpret_cast<const int32_t*>(W1)[k];
   for (int k = tid; k < H; k += NT1) sb1[k] = b1[k];
-  if (warp == 0) tc::tmem_alloc<256>(thold);
-  if (tid == 0) tc::mbar_init(mbar, 1);
+  if (warp == 0) tc::tmem_alloc<512>(thold);
+  if (tid < 2) tc::mbar_init(reinterpret_cast<uint64_t*>(sm + S::MBAR) + tid, 1);
   tc::fence_async_smem();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  const uint32_t tbase = *thold;
-  const uint32_t taddr = tbase + (uint32_t(32 * warp) << 16);  // this thread's TMEM lane
+  const uint32_t tbase = *thold + 256u * uint32_t(tg);                 // the group's 256 columns
+  const uint32_t taddr = tbase + (uint32_t(32 * (warp & 3)) << 16);   // this thread's TMEM lane
   const uint64_t adesc = tc::sdesc(tc::smem_u32(sA));
   const uint64_t bdesc = tc::sdesc(tc::smem_u32(sB));
-  const uint32_t* lutp = reinterpret_cast<const uint32_t*>(sm + S::LUT) + (lane & 3);  // copy lane & 3
+  const uint32_t* lutp = reinterpret_cast<const uint32_t*>(sm + S::LUT) + lane;  // copy `lane`
   const uint32_t ntiles = (n + TILE - 1) / TILE;
+  const uint32_t tstride = 2u * gridDim.x;
   const int64_t lhalf = rql.r > 0 ? (int64_t(1) << (rql.r - 1)) : 0;
+  auto bar_group = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(1 + tg) : "memory"); };
   uint32_t phase = 0;
 
   // the thread's node row F (C bytes) of tile tl, as C/4 words
   auto load_f = [&](uint32_t tl, uint32_t (&fw)[CW]) {
-    const uint32_t rw = tl * TILE + uint32_t(tid);
+    const uint32_t rw = tl * TILE + uint32_t(r);
     if (tl < ntiles && rw < n) {
       const uint32_t* src = reinterpret_cast<const uint32_t*>(F + size_t(rw) * C);
       if constexpr (CW % 4 == 0) {
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(NT1, 2) k_head1_tc(const int8_t* __restrict__ 
   };
   // hidden layer of the thread's node into the A operand (and aw), then b2 into its TMEM lane
   auto hidden_and_bias = [&](uint32_t tl, const uint32_t (&fw)[CW], uint32_t (&aw)[HW]) {
-    const uint32_t rw = tl * TILE + uint32_t(tid);
+    const uint32_t rw = tl * TILE + uint32_t(r);
 #pragma unroll
     for (int g4 = 0; g4 < HW; ++g4) {
       int32_t hacc[4];
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(NT1, 2) k_head1_tc(const int8_t* __restrict__ 
       else
         aw[g4] = (uint32_t(rq8(hacc[0], rq1)) & 0xffu) | (uint32_t(rq8(hacc[1], rq1)) & 0xffu) << 8 |
                  (uint32_t(rq8(hacc[2], rq1)) & 0xffu) << 16 | (uint32_t(rq8(hacc[3], rq1)) & 0xffu) << 24;
-      *reinterpret_cast<uint32_t*>(sA + tc::kmaj_off(uint32_t(tid), 4 * g4)) = aw[g4];
+      *reinterpret_cast<uint32_t*>(sA + tc::kmaj_off(uint32_t(r), 4 * g4)) = aw[g4];
     }
     if (a_dbg && rw < n) {
 #pragma unroll
@@ -172,18 +173,19 @@ __global__ void __launch_bounds__(NT1, 2) k_head1_tc(const int8_t* __restrict__ 
   };
 
   uint32_t fw[CW], aw[HW];
-  load_f(blockIdx.x, fw);
-  if (blockIdx.x < ntiles) hidden_and_bias(blockIdx.x, fw, aw);
-  load_f(blockIdx.x + gridDim.x, fw);
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t row = tile * TILE + uint32_t(tid);
+  const uint32_t t0 = 2u * blockIdx.x + uint32_t(tg);
+  load_f(t0, fw);
+  if (t0 < ntiles) hidden_and_bias(t0, fw, aw);
+  load_f(t0 + tstride, fw);
+  for (uint32_t tile = t0; tile < ntiles; tile += tstride) {
+    const uint32_t row = tile * TILE + uint32_t(r);
     const bool valid = row < n;
-    // A operand (all 128 rows) and the bias-initialised accumulator are complete
+    // the group's A operand (128 rows) and its bias-initialised accumulator are complete
     tc::fence_async_smem();
     tc::fence_before();
-    __syncthreads();
+    bar_group();
     tc::fence_after();
-    if (tid == 0) {
+    if (r == 0) {
       tc::mma_i8(tbase, adesc, bdesc, IDESC, 1u);
       tc::commit(mbar);
     }
@@ -194,18 +196,16 @@ __global__ void __launch_bounds__(NT1, 2) k_head1_tc(const int8_t* __restrict__ 
     // ---- pass 1: max z (and min z) over the 255 symbols (column 255 is padding) ----
     int32_t zmx = INT32_MIN, zmn = INT32_MAX;
 #pragma unroll 1
-    for (int ch = 0; ch < 16; ++ch) {
-      uint32_t v[16];
-      ld16(taddr + ch * 16, v);
+    for (int ch = 0; ch < 8; ++ch) {
+      uint32_t v[32];
+      tc::tmem_ld32(taddr + ch * 32, v);
       tc::tmem_wait_ld();
-      const bool pad = ch == 15;
+      if (ch == 7) v[31] = v[30];  // column 255 is padding, not a symbol
 #pragma unroll
-      for (int k = 0; k < 15; ++k) {
+      for (int k = 0; k < 32; ++k) {
         zmx = max(zmx, int32_t(v[k]));
         if (SAT) zmn = min(zmn, int32_t(v[k]));
       }
-      zmx = max(zmx, pad ? INT32_MIN : int32_t(v[15]));
-      if (SAT) zmn = min(zmn, pad ? INT32_MAX : int32_t(v[15]));
     }
     const int32_t mu = lq8(zmx, rql);
     const bool nosat = !SAT || (zmx <= zsat_hi && zmn >= zsat_lo);
@@ -214,64 +214,68 @@ __global__ void __launch_bounds__(NT1, 2) k_head1_tc(const int8_t* __restrict__ 
     const int64_t C2 = (int64_t(mu) << 32) + 0x7fffffff;
     const int sym = (MODE == 0 && valid) ? int(X[row]) - 1 : 0;
 
-    // ---- pass 2: e_i = LUT[(mu - l_i) >> 2], chunk sums, the encoder's prefix mass ----
-    uint32_t S = 0, pre = 0, es = 0;
+    // ---- pass 2: e_i = LUT[(mu - l_i) >> 2], 16-symbol block sums, the encoder's prefix mass ----
+    uint32_t Sacc = 0, pre = 0, es = 0;
     uint32_t Eb[16];  // decoder: prefix mass before each 16-symbol block
 #pragma unroll 1
-    for (int ch = 0; ch < 16; ++ch) {
-      uint32_t v[16];
-      ld16(taddr + ch * 16, v);
+    for (int ch = 0; ch < 8; ++ch) {
+      uint32_t v[32];
+      tc::tmem_ld32(taddr + ch * 32, v);
       tc::tmem_wait_ld();
       if (fastl) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < 32; ++k) {
           const uint32_t dl = uint32_t(int32_t((int64_t(int32_t(v[k])) * nM + C2) >> 32));
-          v[k] = lutp[4u * min(dl, 4096u)];
+          v[k] = lutp[(min(dl, 4096u) >> 2) * 32u];
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < 32; ++k) {
           const int32_t zz = int32_t(v[k]);
           int32_t lv = int32_t((int64_t(zz) * int64_t(rql.mp) + lhalf) >> rql.r);
           if (SAT && !nosat) {
             lv = zz > zsat_hi ? (1 << 24) : lv;
             lv = zz < zsat_lo ? -(1 << 24) : lv;
           }
-          v[k] = lutp[4u * min(uint32_t(mu - lv), 4096u)];
+          v[k] = lutp[(min(uint32_t(mu - lv), 4096u) >> 2) * 32u];
         }
       }
-      if (ch == 15) v[15] = 0u;  // column 255 is padding, not a symbol
-      uint32_t cs = 0;
+      if (ch == 7) v[31] = 0u;  // column 255 is padding, not a symbol
 #pragma unroll
-      for (int k = 0; k < 16; ++k) cs += v[k];
-      if constexpr (MODE == 0) {
-        const int i0 = 16 * ch;
-        if (sym >= i0 + 16) {
-          pre += cs;
-        } else if (sym >= i0) {
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t cs = 0;
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            pre += (i0 + k < sym) ? v[k] : 0u;
-            es = (i0 + k == sym) ? v[k] : es;
+        for (int k = 0; k < 16; ++k) cs += v[16 * hf + k];
+        if constexpr (MODE == 0) {
+          const int i0 = 32 * ch + 16 * hf;
+          if (sym >= i0 + 16) {
+            pre += cs;
+          } else if (sym >= i0) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              pre += (i0 + k < sym) ? v[16 * hf + k] : 0u;
+              es = (i0 + k == sym) ? v[16 * hf + k] : es;
+            }
           }
+        } else {
+          Eb[2 * ch + hf] = Sacc;
         }
-      } else {
-        Eb[ch] = S;
+        Sacc += cs;  // <= 255 * 2^24 < 2^32
       }
-      S += cs;  // <= 255 * 2^24 < 2^32
     }
+    const uint32_t Ssum = Sacc;
     // all of this thread's TMEM reads are done: the next tile may be set up
     if constexpr (MODE == 0) {
       if (valid) {  // (cum, freq) = (C_sym, C_{sym+1} - C_sym), reading Q21
-        const uint32_t c0 = uint32_t(sym) + uint32_t((uint64_t(pre) * 65281ull) / S);
-        const uint32_t c1 = uint32_t(sym) + 1u + uint32_t((uint64_t(pre + es) * 65281ull) / S);
+        const uint32_t c0 = uint32_t(sym) + uint32_t((uint64_t(pre) * 65281ull) / Ssum);
+        const uint32_t c1 = uint32_t(sym) + 1u + uint32_t((uint64_t(pre + es) * 65281ull) / Ssum);
         cf[row] = c0 | ((c1 - c0) << 16);
       }
     } else if (valid) {
       // decoder row (pcc_internal.cuh DROW_*): S, inv32, mu, E_{16k} k = 1..15, 0, 0, a
       uint4* dst = reinterpret_cast<uint4*>(rows + size_t(row) * DROW_BYTES);
-      const uint32_t inv32 = uint32_t((65281ull << 32) / uint64_t(S));
-      dst[0] = make_uint4(S, inv32, uint32_t(mu), Eb[1]);
+      const uint32_t inv32 = uint32_t((65281ull << 32) / uint64_t(Ssum));
+      dst[0] = make_uint4(Ssum, inv32, uint32_t(mu), Eb[1]);
       dst[1] = make_uint4(Eb[2], Eb[3], Eb[4], Eb[5]);
       dst[2] = make_uint4(Eb[6], Eb[7], Eb[8], Eb[9]);
       dst[3] = make_uint4(Eb[10], Eb[11], Eb[12], Eb[13]);
@@ -283,14 +287,14 @@ __global__ void __launch_bounds__(NT1, 2) k_head1_tc(const int8_t* __restrict__ 
       dst[6] = make_uint4(ap[4], ap[5], ap[6], ap[7]);
     }
     // next tile: hidden layer into A (this tile's MMA has completed) and b2 into TMEM
-    if (tile + gridDim.x < ntiles) {
-      hidden_and_bias(tile + gridDim.x, fw, aw);
-      load_f(tile + 2 * gridDim.x, fw);
+    if (tile + tstride < ntiles) {
+      hidden_and_bias(tile + tstride, fw, aw);
+      load_f(tile + 2 * tstride, fw);
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<256>(tbase);
+  if (warp == 0) tc::tmem_dealloc<512>(*thold);
 }
 
 template <int C, int H, int MODE, bool SAT>
@@ -299,7 +303,7 @@ void launch_head1(pcc_ctx c, const int8_t* F, uint32_t n, const DHead& L, const 
   auto kern = k_head1_tc<C, H, MODE, SAT>;
   PCC_SMEM_ATTR(kern, Smem1::END);
   const uint32_t ntiles = (n + TILE - 1) / TILE;
-  const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * 2u));
+  const unsigned grid = std::max(1u, std::min((ntiles + 1) / 2, unsigned(c->sm_count)));
   kern<<<grid, NT1, Smem1::END, c->stream>>>(F, n, L.W1, L.b1, L.rq1, L.W2, L.b2, L.rql, lut, X, cf,
                                             reinterpret_cast<uint8_t*>(rows), a_dbg, L.zsat_lo, L.zsat_hi);
   launched(c);
