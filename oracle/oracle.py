@@ -112,9 +112,12 @@ class Model:
         return int(lib().oracle_model_hash(self.h))
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().oracle_model_free(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().oracle_model_free(self.h)
+                self.h = None
+        except Exception:  # interpreter shutdown: the library may already be gone
+            pass
 
 
 class Dump:
@@ -134,9 +137,12 @@ class Dump:
         return np.frombuffer(ct.string_at(p.value, n), dtype=dtype).copy()
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().oracle_dump_free(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().oracle_dump_free(self.h)
+                self.h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 def build_octree(xyz: np.ndarray, L: int) -> Tuple[list, list]:

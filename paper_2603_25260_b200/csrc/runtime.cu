@@ -115,11 +115,13 @@ void head_any(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead&
     const char* e = getenv("PCC_HEAD");
     if (e && std::string(e) == "simt") return 2;
     if (e && std::string(e) == "q4") return 1;
+    if (e && std::string(e) == "t1") return 3;
     return 0;
   }();
   if (which == 2) head_cdf(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
   else if (which == 1) head_cdf_tc(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
-  else head_cdf_tc1(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
+  else if (which == 3) head_cdf_tc1(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
+  else head_cdf_tc2(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
 }
 
 inline int lanes_for(uint32_t n) {
