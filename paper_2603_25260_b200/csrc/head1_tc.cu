@@ -107,7 +107,23 @@ __global__ void __launch_bounds__(NT1, 1) k_head1_tc(const int8_t* __restrict__ 
   const uint32_t taddr = tbase + (uint32_t(32 * (warp & 3)) << 16);   // this thread's TMEM lane
   const uint64_t adesc = tc::sdesc(tc::smem_u32(sA));
   const uint64_t bdesc = tc::sdesc(tc::smem_u32(sB));
-  const uint32_t* lutp = reinterpret_cast<const uint32_t*>(sm + S::LUT) + lane;  // copy `lane`
+  // word 32 idx + lane of the 32-copy table: byte offset ((min(delta, 4096) << 5) & ~127) | 4 lane
+  const uint8_t* lutb = sm + S::LUT;
+  const uint32_t lane4 = 4u * uint32_t(lane);
+  auto lut_e = [&](uint32_t dl) -> uint32_t {
+    const uint32_t off = (min(dl << 5, 4096u << 5) & ~127u) | lane4;  // dl < 2^26: no overflow
+    return *reinterpret_cast<const uint32_t*>(lutb + off);
+  };
+  // fast form: X = z * (-M) + mu 2^32 + 2^31 - 1 >= 0 and delta = X >> 32; y = X >> 27 =
+  // 32 delta + (0..31), and (min(y, 4096 * 32) & ~127) is exactly ((min(delta, 4096) >> 2) << 7)
+  const uint32_t lutu = tc::smem_u32(lutb);
+  auto lut_e_fast = [&](int32_t z, int32_t nM, int64_t C2) -> uint32_t {
+    const uint32_t y = uint32_t(uint64_t(int64_t(z) * nM + C2) >> 27);
+    const uint32_t off = (min(y, 4096u << 5) & ~127u) | lane4;
+    uint32_t e;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(lutu + off));
+    return e;
+  };
   const uint32_t ntiles = (n + TILE - 1) / TILE;
   const uint32_t tstride = 2u * gridDim.x;
   const int64_t lhalf = rql.r > 0 ? (int64_t(1) << (rql.r - 1)) : 0;
@@ -225,8 +241,7 @@ __global__ void __launch_bounds__(NT1, 1) k_head1_tc(const int8_t* __restrict__ 
       if (fastl) {
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
-          const uint32_t dl = uint32_t(int32_t((int64_t(int32_t(v[k])) * nM + C2) >> 32));
-          v[k] = lutp[(min(dl, 4096u) >> 2) * 32u];
+          v[k] = lut_e_fast(int32_t(v[k]), nM, C2);
         }
       } else {
 #pragma unroll
@@ -237,7 +252,7 @@ __global__ void __launch_bounds__(NT1, 1) k_head1_tc(const int8_t* __restrict__ 
             lv = zz > zsat_hi ? (1 << 24) : lv;
             lv = zz < zsat_lo ? -(1 << 24) : lv;
           }
-          v[k] = lutp[(min(uint32_t(mu - lv), 4096u) >> 2) * 32u];
+          v[k] = lut_e(uint32_t(mu - lv));
         }
       }
       if (ch == 7) v[31] = 0u;  // column 255 is padding, not a symbol

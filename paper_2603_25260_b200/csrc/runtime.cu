@@ -107,21 +107,23 @@ namespace {
 inline unsigned cdiv(size_t a, size_t b) { return unsigned((a + b - 1) / b); }
 
 // Predictor + softmax: the one-thread-per-node tcgen05 kernel (head1_tc.cu) by default;
-// PCC_HEAD=q4 selects the round-1 tcgen05 kernel (4 threads per node), PCC_HEAD=simt the
-// dp4a warp-per-node kernel (A/B baselines; all are bit-exact).
+// PCC_HEAD=t2 selects the two-threads-per-node kernel (head2_tc.cu), q4 the round-1
+// tcgen05 kernel (4 threads per node), simt the dp4a warp-per-node kernel (A/B baselines;
+// all are bit-exact; measured per 1024-frame cfg2 step: head1 9.7 / 11.7 ms dec / enc,
+// head2 10.5 / 11.6, q4 12.9 / 12.5).
 void head_any(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
               const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg) {
   static const int which = [] {
     const char* e = getenv("PCC_HEAD");
     if (e && std::string(e) == "simt") return 2;
     if (e && std::string(e) == "q4") return 1;
-    if (e && std::string(e) == "t1") return 3;
+    if (e && std::string(e) == "t2") return 3;
     return 0;
   }();
   if (which == 2) head_cdf(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
   else if (which == 1) head_cdf_tc(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
-  else if (which == 3) head_cdf_tc1(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
-  else head_cdf_tc2(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
+  else if (which == 3) head_cdf_tc2(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
+  else head_cdf_tc1(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
 }
 
 inline int lanes_for(uint32_t n) {
