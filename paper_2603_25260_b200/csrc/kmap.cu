@@ -80,6 +80,32 @@ __global__ void k_kmap(const uint64_t* __restrict__ keys, uint32_t n, int depth,
   nbr[t] = r;
 }
 
+// Kernel map of depth d derived from the parent level's (no hashing): the neighbour of
+// node i at offset delta is a child of the parent's neighbour.  Per axis, with the node's
+// child bit b and offset o in {-1, 0, 1}: t = b + o, parent offset floor(t / 2), child bit
+// t & 1.  The child exists iff its bit is set in the parent neighbour's code X, and its
+// row is cs[p'] + popc(X & ((1 << c') - 1)) (children in ascending child index, Q8).
+// Frames never mix: a parent's neighbours are in its own frame.
+__global__ void k_kmap_derive(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ par, uint32_t n,
+                              const int32_t* __restrict__ pnbr, uint32_t np, const uint8_t* __restrict__ Xp,
+                              const uint32_t* __restrict__ csp, int32_t* __restrict__ nbr) {
+  const size_t t = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= size_t(n) * 27) return;
+  const uint32_t i = uint32_t(t / 27), dl = uint32_t(t % 27);
+  const uint32_t c = uint32_t(keys[i] & 7u);
+  const int ox = int(dl / 9) - 1, oy = int((dl / 3) % 3) - 1, oz = int(dl % 3) - 1;
+  const int tx = int(c >> 2) + ox, ty = int((c >> 1) & 1u) + oy, tz = int(c & 1u) + oz;  // in -1..2
+  const int px = (tx + 2) / 2 - 1, py = (ty + 2) / 2 - 1, pz = (tz + 2) / 2 - 1;        // floor(t / 2)
+  const uint32_t cc = uint32_t(((tx & 1) << 2) | ((ty & 1) << 1) | (tz & 1));
+  const int32_t q = pnbr[size_t(par[i]) * 27 + uint32_t((px + 1) * 9 + (py + 1) * 3 + (pz + 1))];
+  int32_t r = int32_t(n);
+  if (q != int32_t(np)) {
+    const uint32_t x = Xp[q];
+    if ((x >> cc) & 1u) r = int32_t(csp[q] + __popc(x & ((1u << cc) - 1u)));
+  }
+  nbr[t] = r;
+}
+
 // HRCS statistic (Fig.1c; SPEC hrcs_stats S:158-166): per node, the number of
 // occupied coordinates among its 26 neighbours at the same depth (exact hash membership).
 // Per-frame sums: the frame id sits above bit 3d of the key, and lanes of a warp holding
@@ -117,6 +143,15 @@ __global__ void k_hrcs(const uint64_t* __restrict__ keys, uint32_t n, int depth,
 }
 
 }  // namespace
+
+void kernel_map_derive(pcc_ctx c, const uint64_t* keys, const uint32_t* par, uint32_t N, const int32_t* pnbr,
+                       uint32_t Np, const uint8_t* Xp, const uint32_t* csp, int32_t* nbr) {
+  if (N == 0) return;
+  const size_t t = size_t(N) * 27;
+  Prof p(c, "kmap", size_t(N) * (8 + 4 + 27 * 4) + size_t(Np) * (27 * 4 + 5));
+  k_kmap_derive<<<unsigned((t + 255) / 256), 256, 0, c->stream>>>(keys, par, N, pnbr, Np, Xp, csp, nbr);
+  launched(c);
+}
 
 void kernel_map(pcc_ctx c, const uint64_t* keys, uint32_t N, int depth, int32_t* nbr) {
   if (N == 0) return;

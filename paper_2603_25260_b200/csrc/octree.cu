@@ -344,16 +344,23 @@ __global__ void k_popc(const uint8_t* __restrict__ X, uint32_t n, uint32_t* __re
   if (i < n) out[i] = __popc(uint32_t(X[i]));
 }
 
+// cap: room left in the node arrays (a corrupt stream can decode more children than any
+// valid one; those are dropped and flagged instead of written out of bounds)
 __global__ void k_expand(const uint64_t* __restrict__ key_d, const uint8_t* __restrict__ X, const uint32_t* __restrict__ cs,
-                         uint32_t n, uint64_t* __restrict__ key_c, uint32_t* __restrict__ par_c) {
+                         uint32_t n, uint64_t* __restrict__ key_c, uint32_t* __restrict__ par_c, uint64_t cap,
+                         uint32_t* __restrict__ err) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   uint32_t x = X[p], j = cs[p];
   const uint64_t k = key_d[p] << 3;
   for (int c = 0; c < 8; ++c)
     if ((x >> c) & 1u) {
-      key_c[j] = k | uint64_t(c);
-      par_c[j] = p;
+      if (j < cap) {
+        key_c[j] = k | uint64_t(c);
+        par_c[j] = p;
+      } else if (err) {
+        atomicOr(err, EF_CORRUPT);
+      }
       ++j;
     }
 }
@@ -498,7 +505,7 @@ void build_octree(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int B, in
   o.foff.assign(hf, hf + size_t(L + 1) * (B + 1));
 }
 
-uint32_t expand_level(pcc_ctx c, int d, int B, OctreeOut& o, uint32_t max_nodes) {
+uint32_t expand_level(pcc_ctx c, int d, int B, OctreeOut& o, uint32_t max_nodes, const uint32_t* err) {
   cudaStream_t s = c->stream;
   const uint32_t n = o.N[d];
   uint64_t* key_all = static_cast<uint64_t*>(c->bufs.at("key").p);
@@ -515,20 +522,17 @@ uint32_t expand_level(pcc_ctx c, int d, int B, OctreeOut& o, uint32_t max_nodes)
   }
   scan_u32(c, tmp, tmp, n);
   PCC_CUDA(cudaMemcpyAsync(cs, tmp, (size_t(n) + 1) * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-  uint32_t* hn = static_cast<uint32_t*>(pinned(c, 4));
-  PCC_CUDA(cudaMemcpyAsync(hn, tmp + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  PCC_CUDA(cudaStreamSynchronize(s));
-  const uint32_t nn = *hn;
-  if (nn > max_nodes) throw Error{PCC_ERR_CORRUPT};
-  o.N.resize(d + 2);
-  o.N[d + 1] = nn;
-  o.nb.resize(d + 3);
-  o.nb[d + 2] = o.nb[d + 1] + nn;
-  if (o.nb[d + 2] > c->bufs.at("key").cap / sizeof(uint64_t)) throw Error{PCC_ERR_CORRUPT};
+  // children are written without knowing their count on the host: the node arrays' room
+  // bounds the writes (k_expand flags anything beyond it)
+  const uint64_t room_keys = c->bufs.at("key").cap / sizeof(uint64_t);
+  const uint64_t room_par = c->bufs.at("par").cap / sizeof(uint32_t);
+  const uint64_t room = std::min(room_keys, room_par);
+  const uint64_t cap = room > o.nb[d + 1] ? room - o.nb[d + 1] : 0;
+  uint32_t* eflag = const_cast<uint32_t*>(err);
   {
-    Prof pe(c, "expand", size_t(n) * 13 + size_t(nn) * 12);
+    Prof pe(c, "expand", size_t(n) * 13);
     k_expand<<<cdiv(n, 256), 256, 0, s>>>(key_all + o.nb[d], code_all + o.nb[d], cs, n, key_all + o.nb[d + 1],
-                                          par_all + o.nb[d + 1]);
+                                          par_all + o.nb[d + 1], cap, eflag);
     launched(c);
   }
   {
@@ -536,11 +540,21 @@ uint32_t expand_level(pcc_ctx c, int d, int B, OctreeOut& o, uint32_t max_nodes)
     k_foff_next<<<cdiv(B + 1, 256), 256, 0, s>>>(cs, d_foff + size_t(d) * (B + 1), B, d_foff + size_t(d + 1) * (B + 1));
     launched(c);
   }
-  uint32_t* hf = static_cast<uint32_t*>(pinned(c, (B + 1) * sizeof(uint32_t)));
-  PCC_CUDA(cudaMemcpyAsync(hf, d_foff + size_t(d + 1) * (B + 1), (B + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  // ONE readback per level: the child count, the error flags (this level's rANS decode and
+  // the expansion), and the per-frame child offsets
+  uint32_t* hb = static_cast<uint32_t*>(pinned(c, (B + 3) * sizeof(uint32_t)));
+  PCC_CUDA(cudaMemcpyAsync(hb, tmp + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  if (err) PCC_CUDA(cudaMemcpyAsync(hb + 1, err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  PCC_CUDA(cudaMemcpyAsync(hb + 2, d_foff + size_t(d + 1) * (B + 1), (B + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   PCC_CUDA(cudaStreamSynchronize(s));
+  const uint32_t nn = hb[0];
+  if ((err && hb[1]) || nn > max_nodes || nn > cap) throw Error{PCC_ERR_CORRUPT};
+  o.N.resize(d + 2);
+  o.N[d + 1] = nn;
+  o.nb.resize(d + 3);
+  o.nb[d + 2] = o.nb[d + 1] + nn;
   o.foff.resize(size_t(d + 2) * (B + 1));
-  for (int f = 0; f <= B; ++f) o.foff[size_t(d + 1) * (B + 1) + f] = hf[f];
+  for (int f = 0; f <= B; ++f) o.foff[size_t(d + 1) * (B + 1) + f] = hb[2 + f];
   return nn;
 }
 

@@ -115,6 +115,8 @@ struct pcc_ctx_s {
   std::map<std::string, Buf> bufs;
   void* pinned = nullptr;
   size_t pinned_cap = 0;
+  void* pinned1 = nullptr;   // second pinned staging buffer (the decoder's segment-list ring)
+  size_t pinned1_cap = 0;
   bool debug = false;
   std::map<std::string, std::vector<uint8_t>> dbg;
   uint64_t launches = 0;
@@ -168,6 +170,7 @@ T* wsT(pcc_ctx c, const char* name, size_t count) {
   return static_cast<T*>(ws(c, name, count * sizeof(T) + 16));
 }
 void* pinned(pcc_ctx c, size_t bytes);
+void* pinned_ring(pcc_ctx c, size_t bytes);  // a separate buffer, not shared with pinned()
 void launched(pcc_ctx c, int n = 1);
 
 // Scoped event pair around one launch of category `cat` (only when profiling is on).
@@ -198,7 +201,8 @@ struct OctreeOut {            // concatenated across depths; node arrays indexed
 // "foff" (u32 [(L+1)*(B+1)]).
 void build_octree(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int B, int L, OctreeOut& o);
 // Decoder: expand depth d -> d+1 from decoded codes (arrays as above).  Returns N_{d+1}.
-uint32_t expand_level(pcc_ctx c, int d, int B, OctreeOut& o, uint32_t max_nodes);
+// err (device flags, may be null): read back with the child count in the level's single sync.
+uint32_t expand_level(pcc_ctx c, int d, int B, OctreeOut& o, uint32_t max_nodes, const uint32_t* err = nullptr);
 // Morton-decode depth-L keys of all frames into xyz (frame bits dropped).
 void keys_to_xyz(pcc_ctx c, const uint64_t* keys, size_t n, int L, int32_t* xyz);
 // HRCS: d_sum[f] = sum over frame f's depth-d nodes of occupied 26-neighbours.
@@ -207,6 +211,10 @@ void hrcs_counts(pcc_ctx c, const uint64_t* keys, uint32_t N, int depth, int B, 
 // ---- kmap.cu ----
 // nbr[N][27] for the N nodes of one depth (keys include frame bits); absent -> N.
 void kernel_map(pcc_ctx c, const uint64_t* keys, uint32_t N, int depth, int32_t* nbr);
+// the same map derived from the parent depth's map (pnbr [Np][27], absent = Np), the parent
+// codes Xp and child starts csp (local to depth d) and the nodes' parents par (local)
+void kernel_map_derive(pcc_ctx c, const uint64_t* keys, const uint32_t* par, uint32_t N, const int32_t* pnbr,
+                       uint32_t Np, const uint8_t* Xp, const uint32_t* csp, int32_t* nbr);
 
 // ---- nn.cu ----
 void embed(pcc_ctx c, const int8_t* E, const uint8_t* X, uint32_t n, int C, int8_t* out);

@@ -45,6 +45,17 @@ void* pinned(pcc_ctx c, size_t bytes) {
 
 // Called after every launch: counts it and surfaces a failed launch (bad configuration,
 // shared-memory limit) immediately instead of as a wrong result later.
+void* pinned_ring(pcc_ctx c, size_t bytes) {
+  if (c->pinned1_cap < bytes) {
+    if (c->pinned1) cudaFreeHost(c->pinned1);
+    c->pinned1 = nullptr;
+    size_t cap = std::max<size_t>(bytes * 2, 1 << 16);
+    PCC_CUDA(cudaMallocHost(&c->pinned1, cap));
+    c->pinned1_cap = cap;
+  }
+  return c->pinned1;
+}
+
 void launched(pcc_ctx c, int n) {
   c->launches += uint64_t(n);
   PCC_CUDA(cudaPeekAtLastError());
@@ -454,8 +465,21 @@ struct Net {
       up_prune(c, S, X(k), par() + o.nb[k + 1], key() + o.nb[k + 1], o.N[k + 1], C, L, dst);
   }
 
+  // depth of the last kernel map built in this call (-1: none): kernel maps are needed at
+  // consecutive depths R-1..D, so every one after the first is derived from its parent's
+  // (kmap.cu k_kmap_derive); PCC_KMAP=hash hashes every depth (A/B baseline)
+  int kmap_last = -1;
   void kmap(int d) {
-    kernel_map(c, key() + o.nb[d], o.N[d], d, nbr(d));
+    static const bool hash_all = [] {
+      const char* e = getenv("PCC_KMAP");
+      return e && std::string(e) == "hash";
+    }();
+    if (!hash_all && d >= 1 && kmap_last == d - 1)
+      kernel_map_derive(c, key() + o.nb[d], par() + o.nb[d], o.N[d], nbr(d - 1), o.N[d - 1], X(d - 1),
+                        cs() + o.nb[d - 1], nbr(d));
+    else
+      kernel_map(c, key() + o.nb[d], o.N[d], d, nbr(d));
+    kmap_last = d;
     if (c->debug) dbg_copy(c, nm("nbr", d), nbr(d), size_t(o.N[d]) * 27 * 4);
   }
 
@@ -940,6 +964,11 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
   }
   // 3. level-serial neural decoding (Eq.2)
   Net net{c, m, L, R, L - 1 - m->n_deep, C, o};
+  // pinned staging for every level's segment list (upper bound: per level, one segment
+  // per frame plus one per 16384 nodes)
+  const size_t seg_ring_cap = size_t(L - R) * ((size_t(B) + NLtot / SEG_SYMS + 2) * sizeof(DecSeg) + 256);
+  uint8_t* seg_ring = static_cast<uint8_t*>(pinned_ring(c, seg_ring_cap));
+  size_t seg_ring_used = 0;
   std::vector<uint64_t> lvl_base(B);
   for (int f = 0; f < B; ++f) lvl_base[f] = bs_offs[f] + 24 + 4 * (L - R) + ((hd[f].raw + 3) & ~3u);
   for (int d = R; d < L; ++d) {
@@ -962,16 +991,20 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
       }
       lvl_base[f] += hd[f].lb[d - R];
     }
-    DecSeg* d_segs = upload(c, "dsegs", segs);
+    // the segment list goes up through its own slice of a per-call pinned ring, so no
+    // level waits for its upload (the level's single sync is the expansion readback)
+    const size_t seg_bytes = segs.size() * sizeof(DecSeg);
+    if (seg_ring_used + seg_bytes > seg_ring_cap) throw Error{PCC_ERR_INVALID_ARG};
+    std::memcpy(seg_ring + seg_ring_used, segs.data(), seg_bytes);
+    DecSeg* d_segs = wsT<DecSeg>(c, "dsegs", segs.size() + 1);
+    PCC_CUDA(cudaMemcpyAsync(d_segs, seg_ring + seg_ring_used, seg_bytes, cudaMemcpyHostToDevice, s));
+    seg_ring_used += (seg_bytes + 255) & ~size_t(255);
     int kmax = 1;
     for (const DecSeg& sg : segs) kmax = std::max(kmax, lanes_for(sg.n));
     rans_decode(c, d_segs, int(segs.size()), d_bs, cdf, m->H, net.head_of(d), m->lut,
                 static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d], err, kmax, nd);
-    PCC_CUDA(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s));
-    PCC_CUDA(cudaStreamSynchronize(s));
-    if (herr) throw Error{PCC_ERR_CORRUPT};
     if (c->debug) dbg_copy(c, nm("code", d), static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d], nd);
-    expand_level(c, d, B, o, uint32_t(std::min<uint64_t>(NLtot, 0xffffffffu)));
+    expand_level(c, d, B, o, uint32_t(std::min<uint64_t>(NLtot, 0xffffffffu)), err);
   }
   for (int f = 0; f < B; ++f)
     if (o.foff[size_t(L) * (B + 1) + f + 1] - o.foff[size_t(L) * (B + 1) + f] != hd[f].NL) throw Error{PCC_ERR_CORRUPT};
@@ -1099,6 +1132,7 @@ void pcc_ctx_destroy(pcc_ctx c) {
   for (auto& kv : c->bufs)
     if (kv.second.p) cudaFree(kv.second.p);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->pinned1) cudaFreeHost(c->pinned1);
   delete c;
 }
 
