@@ -14,6 +14,8 @@
 // accumulator; the identity skip k_s * f is added in the epilogue.  Epilogue: tcgen05.ld
 // of the row's 32 accumulators, bias, skip, PReLU-requant, 32-byte store.
 // Bit-exact with the dp4a kernel and the oracle (int32 addition is associative, O6).
+#include <string>
+
 #include "pcc_internal.cuh"
 #include "rq.cuh"
 #include "tc.cuh"
@@ -284,6 +286,261 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
   if (warp == 0) tc::tmem_dealloc<32>(tmem);
 }
 
+// ---------------------------------------------------------------------------------------
+// Warp-specialised pipeline (the default): 4 gather warps (thread t = output row t of the
+// tile) fill a ring of NS stages (one active kernel offset, or the projection operand, per
+// stage) with cp.async / zero rows and arrive on the stage's FULL mbarrier once their own
+// copies have landed (cp.async.wait_group with NS - 1 stages still in flight per thread);
+// one MMA warp waits FULL, issues the stage's tcgen05.mma(s) and commits to the stage's
+// EMPTY mbarrier, and commits the tile's last MMA to TDONE.  No CTA-wide barrier inside a
+// tile: the gather latency of one offset overlaps the MMAs of the previous ones.  The
+// gather warps then run the epilogue (TMEM -> bias, skip, PReLU-requant -> int8 rows).
+// Stage info (offset, flags) is written by gather thread 0 before its FULL arrival.
+constexpr int WS_NS = 6;  // stages in the ring
+constexpr int WS_NT = 160;  // 4 gather/epilogue warps + 1 MMA warp
+enum : uint32_t { SI_ACC = 1u, SI_LAST = 2u, SI_END = 4u, SI_PROJ = 8u };
+
+template <int SLABS, int SKIP>
+__global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ in0, const int8_t* __restrict__ in1,
+                                                   uint32_t n, const int32_t* __restrict__ nbr,
+                                                   const int8_t* __restrict__ W, const int32_t* __restrict__ bias, RQ rq,
+                                                   const int8_t* __restrict__ skip0, const int8_t* __restrict__ skip1,
+                                                   int32_t k_s, const int8_t* __restrict__ P, int8_t* __restrict__ out) {
+  constexpr int CIN = 32 * SLABS;
+  constexpr int BSLAB = COUT * 32;
+  constexpr int ASLAB = CT * 32;
+  constexpr int B_BYTES = 27 * SLABS * BSLAB;
+  constexpr int P_BYTES = SKIP == 2 ? 2 * BSLAB : 0;
+  constexpr int NS = WS_NS;
+  constexpr int SS = (SKIP == 2) ? 2 : SLABS;  // slabs per stage (the projection stage has 2)
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* sB = sm;
+  uint8_t* sP = sm + B_BYTES;
+  uint8_t* sA = sm + B_BYTES + P_BYTES;                                    // [NS][SS][ASLAB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sA + NS * SS * ASLAB);      // [NS]
+  uint64_t* empty = full + NS;                                             // [NS]
+  uint64_t* tdone = empty + NS;                                            // [1]
+  uint32_t* info = reinterpret_cast<uint32_t*>(tdone + 1);                 // [NS]
+  uint32_t* thold = info + NS;
+  uint32_t* omask2 = thold + 1;  // [2]: by tile parity
+  int32_t* sbias = reinterpret_cast<int32_t*>(thold + 4);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+
+  {  // weights -> canonical K-major slabs (as k_conv3_tc)
+    constexpr int NCH = 27 * COUT * (CIN / 16);
+    for (int k = t; k < NCH; k += WS_NT) {
+      const uint4 v = reinterpret_cast<const uint4*>(W)[k];
+      const int h = k % (CIN / 16), o = (k / (CIN / 16)) % COUT, dl = k / (COUT * (CIN / 16));
+      *reinterpret_cast<uint4*>(sB + (dl * SLABS + h / 2) * BSLAB + tc::kmaj_off(o, 16 * (h % 2))) = v;
+    }
+  }
+  if (SKIP == 2)
+    for (int k = t; k < COUT * 4; k += WS_NT) {
+      const int h = k % 4, o = k / 4;
+      *reinterpret_cast<uint4*>(sP + (h / 2) * BSLAB + tc::kmaj_off(o, 16 * (h % 2))) =
+          reinterpret_cast<const uint4*>(P)[k];
+    }
+  for (int k = t; k < COUT; k += WS_NT) sbias[k] = bias[k];
+  if (warp == 0) tc::tmem_alloc<32>(thold);
+  if (t == 0) {
+    for (int i = 0; i < NS; ++i) {
+      tc::mbar_init(&full[i], CT);
+      tc::mbar_init(&empty[i], 1);
+    }
+    tc::mbar_init(tdone, 1);
+  }
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *thold;
+  const uint32_t ntiles = (n + 1 + CT - 1) / CT;  // rows 0..n (row n = the zero row)
+
+  if (warp == 4) {  // ---- MMA warp: one elected lane issues ----
+    if (lane == 0) {
+      for (uint32_t g = 0;; ++g) {
+        const uint32_t st = g % NS;
+        tc::mbar_wait(&full[st], (g / NS) & 1u);
+        tc::fence_after();
+        const uint32_t inf = info[st];
+        if (inf & SI_END) break;
+        const uint8_t* a = sA + st * SS * ASLAB;
+        const int dl = int(inf >> 8);
+        if (inf & SI_PROJ) {
+          tc::mma_i8(tmem, tc::sdesc(tc::smem_u32(a)), tc::sdesc(tc::smem_u32(sP)), IDESC32, (inf & SI_ACC) ? 1u : 0u);
+          tc::mma_i8(tmem, tc::sdesc(tc::smem_u32(a + ASLAB)), tc::sdesc(tc::smem_u32(sP + BSLAB)), IDESC32, 1u);
+        } else {
+#pragma unroll
+          for (int sl = 0; sl < SLABS; ++sl)
+            tc::mma_i8(tmem, tc::sdesc(tc::smem_u32(a + sl * ASLAB)),
+                       tc::sdesc(tc::smem_u32(sB + (dl * SLABS + sl) * BSLAB)), IDESC32,
+                       ((inf & SI_ACC) || sl > 0) ? 1u : 0u);
+        }
+        tc::commit(&empty[st]);
+        if (inf & SI_LAST) tc::commit(tdone);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- gather / epilogue warps: thread t = row t of the tile ----
+    auto bar_gather = [&]() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+    uint32_t g = 0;          // stage counter (uniform across the gather threads)
+    uint32_t tiles_mma = 0;  // tiles that went through the MMA warp (TDONE phase)
+    int npend = 0;           // stages g - npend .. g - 1 issued by this thread, not yet arrived
+    auto issue_stage = [&](uint32_t inf, const int8_t* s0p, const int8_t* s1p, bool present) {
+      const uint32_t st = g % NS;
+      if (g >= uint32_t(NS)) tc::mbar_wait(&empty[st], ((g / NS) - 1u) & 1u);
+      uint8_t* a = sA + st * SS * ASLAB;
+      if (present) {
+        cp16(a + tc::kmaj_off(t, 0), s0p);
+        cp16(a + tc::kmaj_off(t, 16), s0p + 16);
+        if (SLABS == 2 || (inf & SI_PROJ)) {
+          cp16(a + ASLAB + tc::kmaj_off(t, 0), s1p);
+          cp16(a + ASLAB + tc::kmaj_off(t, 16), s1p + 16);
+        }
+      } else {
+        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int sl = 0; sl < SLABS; ++sl) {
+          *reinterpret_cast<uint4*>(a + sl * ASLAB + tc::kmaj_off(t, 0)) = z;
+          *reinterpret_cast<uint4*>(a + sl * ASLAB + tc::kmaj_off(t, 16)) = z;
+        }
+      }
+      if (t == 0) info[st] = inf;
+      cp_commit();
+      ++npend;
+      if (npend == NS - 1) {  // the oldest stage's copies have landed: hand it to the MMA warp
+        cp_wait<NS - 2>();
+        tc::fence_async_smem();
+        tc::mbar_arrive(&full[(g + 1u - uint32_t(npend)) % NS]);
+        --npend;
+      }
+      ++g;
+    };
+    auto drain = [&]() {
+      cp_wait<0>();
+      tc::fence_async_smem();
+#pragma unroll
+      for (int k = 0; k < NS - 1; ++k)
+        if (k < npend) tc::mbar_arrive(&full[(g - uint32_t(npend) + uint32_t(k)) % NS]);
+      npend = 0;
+    };
+    uint32_t it = 0;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const uint32_t i = tile * CT + uint32_t(t);
+      const bool valid = i < n;
+      uint32_t* omask = omask2 + (it & 1u);
+      if (t == 0) *omask = 0u;
+      bar_gather();
+      uint32_t my = 0;
+      int32_t nb[27];
+#pragma unroll
+      for (int dl = 0; dl < 27; ++dl) {
+        nb[dl] = valid ? nbr[size_t(i) * 27 + dl] : int32_t(n);
+        if (nb[dl] != int32_t(n)) my |= 1u << dl;
+      }
+      my = __reduce_or_sync(0xffffffffu, my);
+      if (lane == 0) atomicOr(omask, my);
+      bar_gather();
+      const uint32_t mask = *omask;
+      const int cnt = __popc(mask) + (SKIP == 2 ? 1 : 0);
+      if (cnt > 0) {
+        int k = 0;
+        for (uint32_t m = mask; m; m &= m - 1, ++k) {
+          const int dl = __ffs(m) - 1;
+          int32_t j = int32_t(n);
+#pragma unroll
+          for (int d2 = 0; d2 < 27; ++d2)
+            if (d2 == dl) j = nb[d2];
+          const uint32_t inf = (uint32_t(dl) << 8) | (k > 0 ? SI_ACC : 0u) | (k == cnt - 1 ? SI_LAST : 0u);
+          issue_stage(inf, in0 + size_t(j) * 32, SLABS == 2 ? in1 + size_t(j) * 32 : nullptr, j != int32_t(n));
+        }
+        if constexpr (SKIP == 2) {  // 1x1 projection of the concat, own row
+          const uint32_t ii = valid ? i : n;
+          issue_stage(SI_PROJ | SI_LAST | (k > 0 ? SI_ACC : 0u), skip0 + size_t(ii) * 32, skip1 + size_t(ii) * 32, true);
+        }
+        drain();
+        tc::mbar_wait(tdone, tiles_mma & 1u);
+        ++tiles_mma;
+        tc::fence_after();
+      }
+      // ---- epilogue ----
+      uint32_t v[32];
+      if (cnt > 0) {
+        tc::tmem_ld32(tmem + (uint32_t(warp * 32) << 16), v);
+        tc::tmem_wait_ld();
+      }
+      if (i <= n) {
+        int32_t acc[32];
+#pragma unroll
+        for (int o = 0; o < 32; ++o) acc[o] = cnt > 0 ? int32_t(v[o]) : 0;
+        uint32_t w[8];
+        if (i < n) {
+          if constexpr (SKIP == 1) {
+            const int4* s4 = reinterpret_cast<const int4*>(skip0 + size_t(i) * 32);
+            const int4 a0 = s4[0], a1 = s4[1];
+            const uint32_t sw[8] = {uint32_t(a0.x), uint32_t(a0.y), uint32_t(a0.z), uint32_t(a0.w),
+                                    uint32_t(a1.x), uint32_t(a1.y), uint32_t(a1.z), uint32_t(a1.w)};
+            if (k_s >= -128 && k_s <= 127) {
+              const int32_t m0 = k_s & 0xff;
+              const int32_t km[4] = {m0, m0 << 8, m0 << 16, int32_t(uint32_t(m0) << 24)};
+#pragma unroll
+              for (int o = 0; o < 32; ++o) acc[o] = __dp4a(int32_t(sw[o >> 2]), km[o & 3], acc[o]);
+            } else {
+#pragma unroll
+              for (int o = 0; o < 32; ++o) acc[o] += k_s * int32_t(int8_t(sw[o >> 2] >> (8 * (o & 3))));
+            }
+          }
+          if (rq.fast_s) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              w[k] = pack_sat4(rq_s(acc[4 * k] + sbias[4 * k], rq), rq_s(acc[4 * k + 1] + sbias[4 * k + 1], rq),
+                               rq_s(acc[4 * k + 2] + sbias[4 * k + 2], rq), rq_s(acc[4 * k + 3] + sbias[4 * k + 3], rq));
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              uint32_t pk = 0;
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                pk |= (uint32_t(rq8(acc[4 * k + u] + sbias[4 * k + u], rq)) & 0xffu) << (8 * u);
+              w[k] = pk;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) w[k] = 0u;  // the zero row
+        }
+        uint4* o4 = reinterpret_cast<uint4*>(out + size_t(i) * 32);
+        o4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        o4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      }
+      tc::fence_before();  // TMEM reads of this tile precede the next tile's MMAs (via FULL)
+    }
+    // tell the MMA warp to stop
+    issue_stage(SI_END, nullptr, nullptr, false);
+    drain();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0) tc::tmem_dealloc<32>(tmem);
+}
+
+template <int SLABS, int SKIP>
+void launch_ws(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,
+               const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out) {
+  constexpr int SS = (SKIP == 2) ? 2 : SLABS;
+  constexpr int smem = 27 * SLABS * 1024 + (SKIP == 2 ? 2048 : 0) + WS_NS * SS * 4096 + (2 * WS_NS + 1) * 8 +
+                       WS_NS * 4 + 16 + 128 + 64;
+  auto kern = k_conv3_ws<SLABS, SKIP>;
+  PCC_SMEM_ATTR(kern, smem);
+  const uint32_t ntiles = (n + 1 + CT - 1) / CT;
+  const int per_sm = std::max(1, 220 * 1024 / smem);
+  const unsigned grid = std::max(1u, std::min(ntiles, unsigned(c->sm_count) * unsigned(per_sm)));
+  Prof p(c, "conv", size_t(n) * (32 * SLABS + 32 + 27 * 4 + (SKIP ? (SKIP == 2 ? 64 : 32) : 0)));
+  kern<<<grid, WS_NT, smem, c->stream>>>(in0, in1, n, nbr, L.W, L.b, L.rq, s0, s1, k_s, P, out);
+  launched(c);
+}
+
 template <int SLABS, int SKIP>
 void launch(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,
             const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out) {
@@ -303,6 +560,24 @@ void launch(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const i
 // C = 32 only (the tcgen05 K slab is 32 channels); other widths use the dp4a kernel.
 void conv3_tc(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,
               int skip_mode, const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out) {
+  // default: the warp-specialised pipeline; PCC_CONV=tc1 keeps the round-1 group kernel
+  static const bool tc1 = [] {
+    const char* e = getenv("PCC_CONV");
+    return e && std::string(e) == "tc1";
+  }();
+  if (!tc1) {
+    if (in1) {
+      if (skip_mode != 0) throw Error{PCC_ERR_INVALID_ARG};
+      launch_ws<2, 0>(c, in0, in1, n, nbr, L, s0, s1, k_s, P, out);
+    } else if (skip_mode == 0) {
+      launch_ws<1, 0>(c, in0, nullptr, n, nbr, L, s0, s1, k_s, P, out);
+    } else if (skip_mode == 1) {
+      launch_ws<1, 1>(c, in0, nullptr, n, nbr, L, s0, s1, k_s, P, out);
+    } else {
+      launch_ws<1, 2>(c, in0, nullptr, n, nbr, L, s0, s1, k_s, P, out);
+    }
+    return;
+  }
   if (in1) {
     if (skip_mode != 0) throw Error{PCC_ERR_INVALID_ARG};
     launch<2, 0>(c, in0, in1, n, nbr, L, s0, s1, k_s, P, out);
