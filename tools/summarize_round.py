@@ -82,8 +82,23 @@ def main(tag):
             dram, dur = summarize(tag, name, os.path.join(OUT, f))
             traffic[name] = {"dram_bytes_per_launch": dram, "launch": "longest launch of one B=256 step",
                              "duration": " ".join(dur) if dur else None, "source": f"profiles/{tag}_ncu_full_{name}.txt"}
-    if traffic:
-        json.dump(traffic, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
+    if traffic:  # keyed by workload (bench.py measured_traffic): these captures are cfg2 steps
+        p = os.path.join(PROF, "traffic.json")
+        try:
+            old = json.load(open(p))
+            old = old if all(isinstance(v, dict) and "dram_bytes_per_launch" not in v for v in old.values()) else {}
+        except Exception:
+            old = {}
+        old["cfg2"] = traffic
+        json.dump(old, open(p, "w"), indent=1)
+    for t in ("memcheck", "racecheck", "synccheck"):
+        p = os.path.join(OUT, f"sanitize_{t}.txt")
+        if os.path.exists(p):
+            keep = [l for l in open(p).read().splitlines()
+                    if l.startswith("ok ") or "SUMMARY" in l or "Error" in l or "ERROR" in l or "Hazard" in l]
+            open(os.path.join(PROF, f"{tag}_sanitize_{t}.txt"), "w").write(
+                f"# compute-sanitizer --tool {t} python tools/sanitize_cfg1.py (cfg1 frame; C = 8 / 32; "
+                "XFP-off, GRED-off and raw-freq models)\n" + "\n".join(keep) + "\n")
     print("wrote", sorted(os.listdir(PROF)))
 
 
