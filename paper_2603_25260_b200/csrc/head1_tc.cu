@@ -37,22 +37,6 @@ __device__ __forceinline__ int32_t lq8(int32_t z, const RQ& q) {  // Q8 logit, c
   return int32_t(v);
 }
 
-__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-}
-// tcgen05.wait::ld that also "defines" v: no use of v can be scheduled before the wait
-__device__ __forceinline__ void wait_ld16(uint32_t (&v)[16]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
-                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
-               :
-               : "memory");
-}
 __device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -225,29 +209,18 @@ __global__ void __launch_bounds__(NT1, 1) k_head1_tc(const int8_t* __restrict__ 
     phase ^= 1u;
     tc::fence_after();
 
-    // TMEM loads are software-pipelined: the next 16 columns are loaded while the current
-    // 16 are processed (tcgen05.wait::ld ties the loaded registers, so no use is hoisted)
     // ---- pass 1: max z (and min z) over the 255 symbols (column 255 is padding) ----
     int32_t zmx = INT32_MIN, zmn = INT32_MAX;
-    auto max16 = [&](uint32_t (&v)[16], int b) {
-      if (b == 15) v[15] = v[14];  // column 255 is padding, not a symbol
+#pragma unroll 1
+    for (int ch = 0; ch < 8; ++ch) {
+      uint32_t v[32];
+      tc::tmem_ld32(taddr + ch * 32, v);
+      tc::tmem_wait_ld();
+      if (ch == 7) v[31] = v[30];  // column 255 is padding, not a symbol
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < 32; ++k) {
         zmx = max(zmx, int32_t(v[k]));
         if (SAT) zmn = min(zmn, int32_t(v[k]));
-      }
-    };
-    {
-      uint32_t va[16], vb[16];
-      ld16(taddr, va);
-#pragma unroll 1
-      for (int b = 0; b < 16; b += 2) {
-        wait_ld16(va);
-        ld16(taddr + (b + 1) * 16, vb);
-        max16(va, b);
-        wait_ld16(vb);
-        if (b + 2 < 16) ld16(taddr + (b + 2) * 16, va);
-        max16(vb, b + 1);
       }
     }
     const int32_t mu = lq8(zmx, rql);
@@ -260,13 +233,19 @@ __global__ void __launch_bounds__(NT1, 1) k_head1_tc(const int8_t* __restrict__ 
     // ---- pass 2: e_i = LUT[(mu - l_i) >> 2], 16-symbol block sums, the encoder's prefix mass ----
     uint32_t Sacc = 0, pre = 0, es = 0;
     uint32_t Eb[16];  // decoder: prefix mass before each 16-symbol block
-    auto exp16 = [&](uint32_t (&v)[16], int b) {  // block b = symbols 16b .. 16b+15
+#pragma unroll 1
+    for (int ch = 0; ch < 8; ++ch) {
+      uint32_t v[32];
+      tc::tmem_ld32(taddr + ch * 32, v);
+      tc::tmem_wait_ld();
       if (fastl) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = lut_e_fast(int32_t(v[k]), nM, C2);
+        for (int k = 0; k < 32; ++k) {
+          v[k] = lut_e_fast(int32_t(v[k]), nM, C2);
+        }
       } else {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < 32; ++k) {
           const int32_t zz = int32_t(v[k]);
           int32_t lv = int32_t((int64_t(zz) * int64_t(rql.mp) + lhalf) >> rql.r);
           if (SAT && !nosat) {
@@ -276,37 +255,27 @@ __global__ void __launch_bounds__(NT1, 1) k_head1_tc(const int8_t* __restrict__ 
           v[k] = lut_e(uint32_t(mu - lv));
         }
       }
-      if (b == 15) v[15] = 0u;  // column 255 is padding, not a symbol
-      uint32_t cs = 0;
+      if (ch == 7) v[31] = 0u;  // column 255 is padding, not a symbol
 #pragma unroll
-      for (int k = 0; k < 16; ++k) cs += v[k];
-      if constexpr (MODE == 0) {
-        const int i0 = 16 * b;
-        if (sym >= i0 + 16) {
-          pre += cs;
-        } else if (sym >= i0) {
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t cs = 0;
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            pre += (i0 + k < sym) ? v[k] : 0u;
-            es = (i0 + k == sym) ? v[k] : es;
+        for (int k = 0; k < 16; ++k) cs += v[16 * hf + k];
+        if constexpr (MODE == 0) {
+          const int i0 = 32 * ch + 16 * hf;
+          if (sym >= i0 + 16) {
+            pre += cs;
+          } else if (sym >= i0) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              pre += (i0 + k < sym) ? v[16 * hf + k] : 0u;
+              es = (i0 + k == sym) ? v[16 * hf + k] : es;
+            }
           }
+        } else {
+          Eb[2 * ch + hf] = Sacc;
         }
-      } else {
-        Eb[b] = Sacc;  // b is a constant: the block loop is fully unrolled
-      }
-      Sacc += cs;  // <= 255 * 2^24 < 2^32
-    };
-    {
-      uint32_t va[16], vb[16];
-      ld16(taddr, va);
-#pragma unroll
-      for (int b = 0; b < 16; b += 2) {
-        wait_ld16(va);
-        ld16(taddr + (b + 1) * 16, vb);
-        exp16(va, b);
-        wait_ld16(vb);
-        if (b + 2 < 16) ld16(taddr + (b + 2) * 16, va);
-        exp16(vb, b + 1);
+        Sacc += cs;  // <= 255 * 2^24 < 2^32
       }
     }
     const uint32_t Ssum = Sacc;
