@@ -238,6 +238,10 @@ void gemm_i8_test(pcc_ctx c, const int8_t* dA, const int8_t* dB, int N, int32_t*
 // ---- head1_tc.cu (same contract; one thread per node, no row barriers: the default) ----
 void head_cdf_tc1(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
                   const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg);
+// ---- head3_tc.cu (same contract; one thread per node, N = 128 half accumulators, ng = 3 or 4
+// tile groups per SM) ----
+void head_cdf_tc3(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
+                  const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg, int ng);
 // ---- head2_tc.cu (same contract; two threads per node, 16 warps per SM) ----
 void head_cdf_tc2(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
                   const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg);

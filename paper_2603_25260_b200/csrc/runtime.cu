@@ -117,11 +117,12 @@ namespace {
 
 inline unsigned cdiv(size_t a, size_t b) { return unsigned((a + b - 1) / b); }
 
-// Predictor + softmax: the one-thread-per-node tcgen05 kernel (head1_tc.cu) by default;
-// PCC_HEAD=t2 selects the two-threads-per-node kernel (head2_tc.cu), q4 the round-1
-// tcgen05 kernel (4 threads per node), simt the dp4a warp-per-node kernel (A/B baselines;
-// all are bit-exact; measured per 1024-frame cfg2 step: head1 9.7 / 11.7 ms dec / enc,
-// head2 10.5 / 11.6, q4 12.9 / 12.5).
+// Predictor + softmax: by default the one-thread-per-node kernel with N = 128 half
+// accumulators and 4 tile groups per SM (head3_tc.cu); PCC_HEAD=t3g3 the same with 3 groups,
+// t1 the full-width one-thread-per-node kernel (head1_tc.cu, 2 groups), t2 two threads per
+// node (head2_tc.cu), q4 the round-1 kernel (4 threads per node), simt the dp4a warp-per-node
+// kernel (A/B baselines; all bit-exact).  Measured per 1024-frame cfg2 step (dec / enc ms):
+// head3 g4 9.5 / 10.4, g3 10.1 / 11.5, head1 9.7 / 11.7, head2 10.5 / 11.6, q4 12.9 / 12.5.
 void head_any(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
               const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg) {
   static const int which = [] {
@@ -129,12 +130,18 @@ void head_any(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead&
     if (e && std::string(e) == "simt") return 2;
     if (e && std::string(e) == "q4") return 1;
     if (e && std::string(e) == "t2") return 3;
-    return 0;
+    if (e && std::string(e) == "t3g3") return 4;
+    if (e && std::string(e) == "t1") return 6;
+    return 5;  // default: head3 with 4 tile groups per SM
   }();
+  if (which == 4 || which == 5) {
+    head_cdf_tc3(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg, which == 4 ? 3 : 4);
+    return;
+  }
   if (which == 2) head_cdf(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
   else if (which == 1) head_cdf_tc(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
   else if (which == 3) head_cdf_tc2(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
-  else head_cdf_tc1(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
+  else head_cdf_tc1(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);  // which == 6
 }
 
 inline int lanes_for(uint32_t n) {
