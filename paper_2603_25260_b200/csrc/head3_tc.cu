@@ -249,17 +249,17 @@ __global__ void __launch_bounds__(NG * 128, 1) k_head3_tc(const int8_t* __restri
     for (int h = 0; h < 2; ++h) {
       mma_half(h);
 #pragma unroll 1
-      for (int b8 = 0; b8 < 8; ++b8) {  // 16-symbol block 8h + b8
-        const int blk = 8 * h + b8;
-        uint32_t v[16];
-        ld16(taddr + b8 * 16, v);
+      for (int ch4 = 0; ch4 < 4; ++ch4) {
+        const int ch = 4 * h + ch4;
+        uint32_t v[32];
+        tc::tmem_ld32(taddr + ch4 * 32, v);
         tc::tmem_wait_ld();
         if (fastl) {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) v[k] = lut_e_fast(int32_t(v[k]), nM, C2);
+          for (int k = 0; k < 32; ++k) v[k] = lut_e_fast(int32_t(v[k]), nM, C2);
         } else {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
+          for (int k = 0; k < 32; ++k) {
             const int32_t zz = int32_t(v[k]);
             int32_t lv = int32_t((int64_t(zz) * int64_t(rql.mp) + lhalf) >> rql.r);
             if (SAT && !nosat) {
@@ -269,27 +269,28 @@ __global__ void __launch_bounds__(NG * 128, 1) k_head3_tc(const int8_t* __restri
             v[k] = lut_e(uint32_t(mu - lv));
           }
         }
-        if (blk == 15) v[15] = 0u;  // column 255 is padding, not a symbol
-        uint32_t cs = 0;
+        if (ch == 7) v[31] = 0u;  // column 255 is padding, not a symbol
 #pragma unroll
-        for (int k = 0; k < 16; ++k) cs += v[k];
-        if constexpr (MODE == 0) {
-          const int i0 = 16 * blk;
-          if (sym >= i0 + 16) {
-            pre += cs;
-          } else if (sym >= i0) {
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t cs = 0;
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              pre += (i0 + k < sym) ? v[k] : 0u;
-              es = (i0 + k == sym) ? v[k] : es;
+          for (int k = 0; k < 16; ++k) cs += v[16 * hf + k];
+          if constexpr (MODE == 0) {
+            const int i0 = 32 * ch + 16 * hf;
+            if (sym >= i0 + 16) {
+              pre += cs;
+            } else if (sym >= i0) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                pre += (i0 + k < sym) ? v[16 * hf + k] : 0u;
+                es = (i0 + k == sym) ? v[16 * hf + k] : es;
+              }
             }
+          } else {
+            Eb[2 * ch + hf] = Sacc;
           }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 16; ++q)
-            if (q == blk) Eb[q] = Sacc;
+          Sacc += cs;  // <= 255 * 2^24 < 2^32
         }
-        Sacc += cs;  // <= 255 * 2^24 < 2^32
       }
     }
     const uint32_t Ssum = Sacc;
