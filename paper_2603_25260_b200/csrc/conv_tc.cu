@@ -290,15 +290,18 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
 // Warp-specialised pipeline (the default): 4 gather warps (thread t = output row t of the
 // tile) fill a ring of NS stages (one active kernel offset, or the projection operand, per
 // stage) with cp.async / zero rows and arrive on the stage's FULL mbarrier once their own
-// copies have landed (cp.async.wait_group with NS - 1 stages still in flight per thread);
-// one MMA warp waits FULL, issues the stage's tcgen05.mma(s) and commits to the stage's
-// EMPTY mbarrier, and commits the tile's last MMA to TDONE.  No CTA-wide barrier inside a
-// tile: the gather latency of one offset overlaps the MMAs of the previous ones.  The
-// gather warps then run the epilogue (TMEM -> bias, skip, PReLU-requant -> int8 rows).
-// Stage info (offset, flags) is written by gather thread 0 before its FULL arrival.
-constexpr int WS_NS = 6;  // stages in the ring
-constexpr int WS_NT = 160;  // 4 gather/epilogue warps + 1 MMA warp
-enum : uint32_t { SI_ACC = 1u, SI_LAST = 2u, SI_END = 4u, SI_PROJ = 8u };
+// copies have landed (cp.async.wait_group with NS - 2 later stages still in flight per
+// thread); one MMA warp waits FULL, issues the stage's tcgen05.mma(s) into one of two TMEM
+// accumulators and commits the stage's EMPTY mbarrier, and the tile's last MMA to
+// TDONE[b]; 4 epilogue warps wait TDONE[b], read the accumulator, release it (TEMPTY[b])
+// and requantise / store the rows.  No CTA-wide barrier inside the tile loop: the gather
+// warps stream stages across tiles while the previous tile's MMAs drain and its epilogue
+// runs.  Stage info (offset, accumulator, flags) is written by gather thread 0 before its
+// FULL arrival.  Tiles with no active offset still run one (zero) stage, so every tile
+// goes through TDONE.
+constexpr int WS_NS = 6;    // stages in the ring
+constexpr int WS_NT = 288;  // 4 gather warps + 1 MMA warp + 4 epilogue warps
+enum : uint32_t { SI_ACC = 1u, SI_LAST = 2u, SI_END = 4u, SI_PROJ = 8u, SI_BUF1 = 16u };
 
 template <int SLABS, int SKIP>
 __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ in0, const int8_t* __restrict__ in1,
@@ -319,8 +322,9 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
   uint8_t* sA = sm + B_BYTES + P_BYTES;                                    // [NS][SS][ASLAB]
   uint64_t* full = reinterpret_cast<uint64_t*>(sA + NS * SS * ASLAB);      // [NS]
   uint64_t* empty = full + NS;                                             // [NS]
-  uint64_t* tdone = empty + NS;                                            // [1]
-  uint32_t* info = reinterpret_cast<uint32_t*>(tdone + 1);                 // [NS]
+  uint64_t* tdone = empty + NS;                                            // [2]
+  uint64_t* tempty = tdone + 2;                                            // [2]
+  uint32_t* info = reinterpret_cast<uint32_t*>(tempty + 2);                // [NS]
   uint32_t* thold = info + NS;
   uint32_t* omask2 = thold + 1;  // [2]: by tile parity
   int32_t* sbias = reinterpret_cast<int32_t*>(thold + 4);
@@ -341,13 +345,16 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
           reinterpret_cast<const uint4*>(P)[k];
     }
   for (int k = t; k < COUT; k += WS_NT) sbias[k] = bias[k];
-  if (warp == 0) tc::tmem_alloc<32>(thold);
+  if (warp == 0) tc::tmem_alloc<64>(thold);  // two 32-column accumulators
   if (t == 0) {
     for (int i = 0; i < NS; ++i) {
       tc::mbar_init(&full[i], CT);
       tc::mbar_init(&empty[i], 1);
     }
-    tc::mbar_init(tdone, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tdone[b], 1);
+      tc::mbar_init(&tempty[b], CT);
+    }
   }
   tc::fence_async_smem();
   tc::fence_before();
@@ -358,34 +365,41 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
 
   if (warp == 4) {  // ---- MMA warp: one elected lane issues ----
     if (lane == 0) {
+      uint32_t tl = 0;  // tiles started (accumulator b = tl & 1)
       for (uint32_t g = 0;; ++g) {
         const uint32_t st = g % NS;
         tc::mbar_wait(&full[st], (g / NS) & 1u);
         tc::fence_after();
         const uint32_t inf = info[st];
         if (inf & SI_END) break;
+        const uint32_t b = (inf & SI_BUF1) ? 1u : 0u;
+        if (!(inf & SI_ACC)) {  // first stage of a tile: its accumulator must be free
+          if (tl >= 2) tc::mbar_wait(&tempty[b], ((tl >> 1) - 1u) & 1u);
+          tc::fence_after();
+          ++tl;
+        }
+        const uint32_t acc_t = tmem + 32u * b;
         const uint8_t* a = sA + st * SS * ASLAB;
         const int dl = int(inf >> 8);
         if (inf & SI_PROJ) {
-          tc::mma_i8(tmem, tc::sdesc(tc::smem_u32(a)), tc::sdesc(tc::smem_u32(sP)), IDESC32, (inf & SI_ACC) ? 1u : 0u);
-          tc::mma_i8(tmem, tc::sdesc(tc::smem_u32(a + ASLAB)), tc::sdesc(tc::smem_u32(sP + BSLAB)), IDESC32, 1u);
+          tc::mma_i8(acc_t, tc::sdesc(tc::smem_u32(a)), tc::sdesc(tc::smem_u32(sP)), IDESC32, (inf & SI_ACC) ? 1u : 0u);
+          tc::mma_i8(acc_t, tc::sdesc(tc::smem_u32(a + ASLAB)), tc::sdesc(tc::smem_u32(sP + BSLAB)), IDESC32, 1u);
         } else {
 #pragma unroll
           for (int sl = 0; sl < SLABS; ++sl)
-            tc::mma_i8(tmem, tc::sdesc(tc::smem_u32(a + sl * ASLAB)),
+            tc::mma_i8(acc_t, tc::sdesc(tc::smem_u32(a + sl * ASLAB)),
                        tc::sdesc(tc::smem_u32(sB + (dl * SLABS + sl) * BSLAB)), IDESC32,
                        ((inf & SI_ACC) || sl > 0) ? 1u : 0u);
         }
         tc::commit(&empty[st]);
-        if (inf & SI_LAST) tc::commit(tdone);
+        if (inf & SI_LAST) tc::commit(&tdone[b]);
       }
     }
     __syncwarp();
-  } else {  // ---- gather / epilogue warps: thread t = row t of the tile ----
+  } else if (warp < 4) {  // ---- gather warps: thread t = row t of the tile ----
     auto bar_gather = [&]() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
-    uint32_t g = 0;          // stage counter (uniform across the gather threads)
-    uint32_t tiles_mma = 0;  // tiles that went through the MMA warp (TDONE phase)
-    int npend = 0;           // stages g - npend .. g - 1 issued by this thread, not yet arrived
+    uint32_t g = 0;   // stage counter (uniform across the gather threads)
+    int npend = 0;    // stages g - npend .. g - 1 issued by this thread, not yet arrived
     auto issue_stage = [&](uint32_t inf, const int8_t* s0p, const int8_t* s1p, bool present) {
       const uint32_t st = g % NS;
       if (g >= uint32_t(NS)) tc::mbar_wait(&empty[st], ((g / NS) - 1u) & 1u);
@@ -428,6 +442,7 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t i = tile * CT + uint32_t(t);
       const bool valid = i < n;
+      const uint32_t bufbit = (it & 1u) ? SI_BUF1 : 0u;
       uint32_t* omask = omask2 + (it & 1u);
       if (t == 0) *omask = 0u;
       bar_gather();
@@ -443,7 +458,9 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
       bar_gather();
       const uint32_t mask = *omask;
       const int cnt = __popc(mask) + (SKIP == 2 ? 1 : 0);
-      if (cnt > 0) {
+      if (cnt == 0) {  // no neighbour anywhere in the tile: one zero stage (accumulator = 0)
+        issue_stage((13u << 8) | SI_LAST | bufbit, nullptr, nullptr, false);
+      } else {
         int k = 0;
         for (uint32_t m = mask; m; m &= m - 1, ++k) {
           const int dl = __ffs(m) - 1;
@@ -451,28 +468,36 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
 #pragma unroll
           for (int d2 = 0; d2 < 27; ++d2)
             if (d2 == dl) j = nb[d2];
-          const uint32_t inf = (uint32_t(dl) << 8) | (k > 0 ? SI_ACC : 0u) | (k == cnt - 1 ? SI_LAST : 0u);
+          const uint32_t inf = (uint32_t(dl) << 8) | bufbit | (k > 0 ? SI_ACC : 0u) | (k == cnt - 1 ? SI_LAST : 0u);
           issue_stage(inf, in0 + size_t(j) * 32, SLABS == 2 ? in1 + size_t(j) * 32 : nullptr, j != int32_t(n));
         }
         if constexpr (SKIP == 2) {  // 1x1 projection of the concat, own row
           const uint32_t ii = valid ? i : n;
-          issue_stage(SI_PROJ | SI_LAST | (k > 0 ? SI_ACC : 0u), skip0 + size_t(ii) * 32, skip1 + size_t(ii) * 32, true);
+          issue_stage(SI_PROJ | SI_LAST | bufbit | (k > 0 ? SI_ACC : 0u), skip0 + size_t(ii) * 32,
+                      skip1 + size_t(ii) * 32, true);
         }
-        drain();
-        tc::mbar_wait(tdone, tiles_mma & 1u);
-        ++tiles_mma;
-        tc::fence_after();
       }
-      // ---- epilogue ----
+    }
+    // tell the MMA warp to stop, and hand over everything still pending
+    issue_stage(SI_END, nullptr, nullptr, false);
+    drain();
+  } else {  // ---- epilogue warps (5..8): TMEM lane quarter warp % 4 ----
+    const int r = 32 * (warp & 3) + lane;
+    uint32_t it = 0;
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const uint32_t b = it & 1u;
+      const uint32_t i = tile * CT + uint32_t(r);
+      tc::mbar_wait(&tdone[b], (it >> 1) & 1u);
+      tc::fence_after();
       uint32_t v[32];
-      if (cnt > 0) {
-        tc::tmem_ld32(tmem + (uint32_t(warp * 32) << 16), v);
-        tc::tmem_wait_ld();
-      }
+      tc::tmem_ld32(tmem + 32u * b + (uint32_t(32 * (warp & 3)) << 16), v);
+      tc::tmem_wait_ld();
+      tc::fence_before();
+      tc::mbar_arrive(&tempty[b]);  // the accumulator may be overwritten now
       if (i <= n) {
         int32_t acc[32];
 #pragma unroll
-        for (int o = 0; o < 32; ++o) acc[o] = cnt > 0 ? int32_t(v[o]) : 0;
+        for (int o = 0; o < 32; ++o) acc[o] = int32_t(v[o]);
         uint32_t w[8];
         if (i < n) {
           if constexpr (SKIP == 1) {
@@ -513,23 +538,19 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
         o4[0] = make_uint4(w[0], w[1], w[2], w[3]);
         o4[1] = make_uint4(w[4], w[5], w[6], w[7]);
       }
-      tc::fence_before();  // TMEM reads of this tile precede the next tile's MMAs (via FULL)
     }
-    // tell the MMA warp to stop
-    issue_stage(SI_END, nullptr, nullptr, false);
-    drain();
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  if (warp == 0) tc::tmem_dealloc<32>(tmem);
+  if (warp == 0) tc::tmem_dealloc<64>(tmem);
 }
 
 template <int SLABS, int SKIP>
 void launch_ws(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,
                const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out) {
   constexpr int SS = (SKIP == 2) ? 2 : SLABS;
-  constexpr int smem = 27 * SLABS * 1024 + (SKIP == 2 ? 2048 : 0) + WS_NS * SS * 4096 + (2 * WS_NS + 1) * 8 +
+  constexpr int smem = 27 * SLABS * 1024 + (SKIP == 2 ? 2048 : 0) + WS_NS * SS * 4096 + (2 * WS_NS + 4) * 8 +
                        WS_NS * 4 + 16 + 128 + 64;
   auto kern = k_conv3_ws<SLABS, SKIP>;
   PCC_SMEM_ATTR(kern, smem);
