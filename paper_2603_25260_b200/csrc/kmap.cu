@@ -2,6 +2,8 @@
 // convolution "decomposed into multiple indexed linear transforms"; the kernel map is the
 // index list of each transform).  Keys carry the frame id above bit 3d, so neighbours
 // never cross frames.  nbr[i][delta] = row of coord(i)+delta, or N (the zero row).
+#include <string>
+
 #include "pcc_internal.cuh"
 
 namespace pcc {
@@ -106,6 +108,58 @@ __global__ void k_kmap_derive(const uint64_t* __restrict__ keys, const uint32_t*
   nbr[t] = r;
 }
 
+// The same derivation with one thread per node: a node's 27 neighbours come from only 8
+// parent neighbours (per axis, offsets -1/0/+1 of a child with bit b fall into parent
+// offsets b-1 and b), so the node loads those 8 parent entries, their codes and child
+// starts once (24 loads instead of 81), builds its 27 entries in shared memory and the
+// block stores 128 rows coalesced.
+__global__ void __launch_bounds__(128) k_kmap_derive8(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ par,
+                                                      uint32_t n, const int32_t* __restrict__ pnbr, uint32_t np,
+                                                      const uint8_t* __restrict__ Xp, const uint32_t* __restrict__ csp,
+                                                      int32_t* __restrict__ nbr) {
+  __shared__ int32_t so[128 * 27];
+  const uint32_t i0 = blockIdx.x * 128u;
+  const uint32_t i = i0 + threadIdx.x;
+  if (i < n) {
+    const uint32_t c = uint32_t(keys[i] & 7u);
+    const int bx = int(c >> 2), by = int((c >> 1) & 1u), bz = int(c & 1u);
+    const int32_t* pn = pnbr + size_t(par[i]) * 27;
+    int32_t q[8];
+    uint32_t qx[8], qc[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {  // parent neighbour (bx - 1 + sx, by - 1 + sy, bz - 1 + sz)
+      const int sx = s >> 2, sy = (s >> 1) & 1, sz = s & 1;
+      q[s] = pn[(bx + sx) * 9 + (by + sy) * 3 + (bz + sz)];
+    }
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const bool ok = q[s] != int32_t(np);
+      qx[s] = ok ? uint32_t(Xp[q[s]]) : 0u;
+      qc[s] = ok ? csp[q[s]] : 0u;
+    }
+#pragma unroll
+    for (int dl = 0; dl < 27; ++dl) {
+      const int ox = dl / 9 - 1, oy = (dl / 3) % 3 - 1, oz = dl % 3 - 1;
+      const int tx = bx + ox, ty = by + oy, tz = bz + oz;  // in -1..2
+      // parent offset floor(t / 2) = b - 1 + side, side = (t + 2) / 2 - b
+      const int s = (((tx + 2) / 2 - bx) << 2) | (((ty + 2) / 2 - by) << 1) | ((tz + 2) / 2 - bz);
+      const uint32_t cc = uint32_t(((tx & 1) << 2) | ((ty & 1) << 1) | (tz & 1));
+      uint32_t x = 0, cs0 = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (u == s) {
+          x = qx[u];
+          cs0 = qc[u];
+        }
+      so[threadIdx.x * 27 + dl] = ((x >> cc) & 1u) ? int32_t(cs0 + __popc(x & ((1u << cc) - 1u))) : int32_t(n);
+    }
+  }
+  __syncthreads();
+  const uint32_t rows = min(128u, n - i0);
+  int32_t* dst = nbr + size_t(i0) * 27;
+  for (uint32_t k = threadIdx.x; k < rows * 27; k += 128) dst[k] = so[k];
+}
+
 // HRCS statistic (Fig.1c; SPEC hrcs_stats S:158-166): per node, the number of
 // occupied coordinates among its 26 neighbours at the same depth (exact hash membership).
 // Per-frame sums: the frame id sits above bit 3d of the key, and lanes of a warp holding
@@ -149,7 +203,14 @@ void kernel_map_derive(pcc_ctx c, const uint64_t* keys, const uint32_t* par, uin
   if (N == 0) return;
   const size_t t = size_t(N) * 27;
   Prof p(c, "kmap", size_t(N) * (8 + 4 + 27 * 4) + size_t(Np) * (27 * 4 + 5));
-  k_kmap_derive<<<unsigned((t + 255) / 256), 256, 0, c->stream>>>(keys, par, N, pnbr, Np, Xp, csp, nbr);
+  static const bool per_pair = [] {
+    const char* e = getenv("PCC_KMAP");
+    return e && std::string(e) == "derive27";
+  }();
+  if (per_pair)
+    k_kmap_derive<<<unsigned((t + 255) / 256), 256, 0, c->stream>>>(keys, par, N, pnbr, Np, Xp, csp, nbr);
+  else
+    k_kmap_derive8<<<unsigned((N + 127) / 128), 128, 0, c->stream>>>(keys, par, N, pnbr, Np, Xp, csp, nbr);
   launched(c);
 }
 
