@@ -24,13 +24,32 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+def _compile(src: str, obj: str, verbose: bool) -> None:
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+           "-Xptxas", "-v" if verbose else "-O3", "-c", "-o", obj, src]
+    subprocess.check_call(cmd, cwd=CSRC)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile each .cu to an object in build/ (in parallel, only the stale ones) and link."""
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+    odir = os.path.join(HERE, "..", "build", "objs")
+    os.makedirs(odir, exist_ok=True)
+    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(HERE, "..", "include", "pcc.h")]
+    th = max(os.path.getmtime(h) for h in hdrs)
+    objs, todo = [], []
+    for src in sources():
+        obj = os.path.join(odir, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(th, os.path.getmtime(src)):
+            todo.append((src, obj))
+    with ThreadPoolExecutor(max_workers=min(len(todo) or 1, os.cpu_count() or 4)) as ex:
+        for f in [ex.submit(_compile, s, o, verbose) for s, o in todo]:
+            f.result()
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3", "-o", tmp, *sources(), "-lcuda"]
-    subprocess.check_call(cmd, cwd=CSRC)
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcuda"], cwd=CSRC)
     os.replace(tmp, LIB)
     return LIB
 

@@ -118,6 +118,17 @@ __global__ void __launch_bounds__(NG * 128, 1) k_head3_tc(const int8_t* __restri
     asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(lutu + off));
     return e;
   };
+  // index form (r <= 30, so 4 | Sp): idx = delta >> 2 = floor(X / 2^34) = hi32(z * (-Sp / 4) +
+  // mu 2^30 + 2^29 - 1) (z * Sp / 4 is an integer, so the floor of C2 / 4 may replace C2 / 4):
+  // the LUT index is the high word of one IMAD.WIDE; the word address is min(idx, 1024) * 128
+  // + 4 lane: one min (alu pipe) and one multiply-add (fma pipe) instead of shift, min, and
+  auto lut_e_idx = [&](int32_t z, int32_t nM4, int64_t C4) -> uint32_t {
+    const uint32_t idx = uint32_t(uint64_t(int64_t(z) * nM4 + C4) >> 32);  // delta >= 0
+    uint32_t off, e;
+    asm("mad.lo.u32 %0, %1, 128, %2;" : "=r"(off) : "r"(min(idx, 1024u)), "r"(lutu + lane4));
+    asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(off));
+    return e;
+  };
   const uint32_t ntiles = (n + TILE - 1) / TILE;
   const uint32_t tstride = uint32_t(NG) * gridDim.x;
   const int64_t lhalf = rql.r > 0 ? (int64_t(1) << (rql.r - 1)) : 0;
@@ -230,8 +241,11 @@ __global__ void __launch_bounds__(NG * 128, 1) k_head3_tc(const int8_t* __restri
     const int32_t mu = lq8(zmx, rql);
     const bool nosat = !SAT || (zmx <= zsat_hi && zmn >= zsat_lo);
     const bool fastl = rql.fast_s && nosat;
+    const bool fasti = fastl && rql.r <= 30;
     const int32_t nM = -rql.Sp;
     const int64_t C2 = (int64_t(mu) << 32) + 0x7fffffff;
+    const int32_t nM4 = -(rql.Sp >> 2);
+    const int64_t C4 = (int64_t(mu) << 30) + ((int64_t(1) << 29) - 1);
     const int sym = (MODE == 0 && valid) ? int(X[row]) - 1 : 0;
 
     // ---- pass 2: e_i = LUT[(mu - l_i) >> 2], 16-symbol block sums, the encoder's prefix mass ----
@@ -246,7 +260,10 @@ __global__ void __launch_bounds__(NG * 128, 1) k_head3_tc(const int8_t* __restri
         uint32_t v[32];
         tc::tmem_ld32(taddr + ch4 * 32, v);
         tc::tmem_wait_ld();
-        if (fastl) {
+        if (fasti) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[k] = lut_e_idx(int32_t(v[k]), nM4, C4);
+        } else if (fastl) {
 #pragma unroll
           for (int k = 0; k < 32; ++k) v[k] = lut_e_fast(int32_t(v[k]), nM, C2);
         } else {
