@@ -60,6 +60,11 @@ struct DHead {       // Predictor: W1 [H][C], b1, rq1; W2 [256][H] (row 255 = 0)
   int32_t zsat_lo, zsat_hi;
   // false when max_i(|b2_i| + 128 sum_h |W2_ih|) is inside both thresholds
   bool can_saturate;
+  // head4_tc.cu: the biases as a second K = 32 MMA slab, b = 127 sum_{j<31} d_j + d_31
+  // (B1d [32][32], rows >= H zero; B2d [256][32], row 255 zero); valid iff bias_fold
+  const int8_t* B1d;
+  const int8_t* B2d;
+  bool bias_fold;
 };
 struct DShallow {
   DConv a, b;
@@ -240,6 +245,8 @@ void head_cdf_tc1(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DH
                   const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg);
 // ---- head3_tc.cu (same contract; one thread per node, N = 128 half accumulators, ng = 3 or 4
 // tile groups per SM) ----
+void head_cdf_tc4(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
+                  const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg);
 void head_cdf_tc3(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead& L, const uint32_t* lut, int mode,
                   const uint8_t* X, uint32_t* cf, uint16_t* cdf, int8_t* a_dbg, int ng);
 // ---- head2_tc.cu (same contract; two threads per node, 16 warps per SM) ----

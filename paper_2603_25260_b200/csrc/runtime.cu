@@ -132,9 +132,14 @@ void head_any(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead&
     if (e && std::string(e) == "t2") return 3;
     if (e && std::string(e) == "t3g3") return 4;
     if (e && std::string(e) == "t1") return 6;
-    return 5;  // default: head3 with 4 tile groups per SM
+    if (e && std::string(e) == "t3") return 5;
+    return 7;  // default: head4 (both layers and biases on tcgen05), head3 if a bias is too large
   }();
-  if (which == 4 || which == 5) {
+  if (which == 7 && L.bias_fold) {
+    head_cdf_tc4(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
+    return;
+  }
+  if (which == 4 || which == 5 || which == 7) {
     head_cdf_tc3(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg, which == 4 ? 3 : 4);
     return;
   }
@@ -142,6 +147,25 @@ void head_any(pcc_ctx c, const int8_t* F, uint32_t n, int C, int H, const DHead&
   else if (which == 1) head_cdf_tc(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
   else if (which == 3) head_cdf_tc2(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);
   else head_cdf_tc1(c, F, n, C, H, L, lut, mode, X, cf, cdf, a_dbg);  // which == 6
+}
+
+// b = 127 sum_{j<31} d_j + d_31 with |d_j| <= 127 and d_31 = b mod 127 in [0, 126], one
+// row of 32 digits per bias; false when some |b| is too large for 31 digits
+bool bias_digits(const std::vector<int32_t>& b, std::vector<int8_t>& D) {
+  D.assign(b.size() * 32, 0);
+  for (size_t i = 0; i < b.size(); ++i) {
+    const int64_t v = b[i];
+    const int64_t rem = ((v % 127) + 127) % 127;
+    int64_t q = (v - rem) / 127;
+    if (q > 31 * 127 || q < -31 * 127) return false;
+    for (int j = 0; j < 31; ++j) {
+      const int64_t d = q > 127 ? 127 : (q < -127 ? -127 : q);
+      D[i * 32 + j] = int8_t(d);
+      q -= d;
+    }
+    D[i * 32 + 31] = int8_t(rem);
+  }
+  return true;
 }
 
 inline int lanes_for(uint32_t n) {
@@ -320,7 +344,10 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
     auto head = [&]() {
       DHead hd;
       hd.W1 = off_ptr<const int8_t>(st.put(r.take(size_t(H) * C), size_t(H) * C));
-      hd.b1 = off_ptr<const int32_t>(st.put(r.take(size_t(4) * H), size_t(4) * H));
+      const uint8_t* b1p = r.take(size_t(4) * H);
+      std::vector<int32_t> hd_b1_host(H);
+      std::memcpy(hd_b1_host.data(), b1p, size_t(4) * H);
+      hd.b1 = off_ptr<const int32_t>(st.put(b1p, size_t(4) * H));
       hd.rq1 = r.rq();
       std::vector<int8_t> W2(size_t(256) * H, 0);
       std::memcpy(W2.data(), r.take(size_t(NCODE) * H), size_t(NCODE) * H);
@@ -339,6 +366,14 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
       }
       hd.W2 = off_ptr<const int8_t>(st.put(W2.data(), W2.size()));
       hd.b2 = off_ptr<const int32_t>(st.put(b2.data(), b2.size() * 4));
+      {  // bias digits for head4_tc.cu: b = 127 sum_{j<31} d_j + d_31, d_31 = b mod 127
+        std::vector<int32_t> b1(32, 0);
+        std::memcpy(b1.data(), hd_b1_host.data(), size_t(4) * H);
+        std::vector<int8_t> D1, D2;
+        hd.bias_fold = bias_digits(b1, D1) && bias_digits(b2, D2);
+        hd.B1d = off_ptr<const int8_t>(st.put(D1.data(), D1.size()));
+        hd.B2d = off_ptr<const int8_t>(st.put(D2.data(), D2.size()));
+      }
       return hd;
     };
     for (int d = m->R; d < m->max_depth - m->n_deep; ++d) {
@@ -390,6 +425,7 @@ pcc_model load_model(const uint8_t* bytes, size_t len, int device) {
     m->E0 = reinterpret_cast<const int8_t*>(base + o_E0);
     auto rb_head = [&](DHead& hd) {
       hd.W1 = rebase(hd.W1, base); hd.b1 = rebase(hd.b1, base); hd.W2 = rebase(hd.W2, base); hd.b2 = rebase(hd.b2, base);
+      hd.B1d = rebase(hd.B1d, base); hd.B2d = rebase(hd.B2d, base);
     };
     auto rb_up = [&](DUp& u) {
       u.W = rebase(u.W, base); u.E = rebase(u.E, base); u.b = rebase(u.b, base); u.WXt = rebase(u.WXt, base);

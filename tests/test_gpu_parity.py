@@ -474,7 +474,7 @@ print("ALT-OK")
 @pytest.mark.parametrize("env", [{"PCC_UP": "simt", "PCC_DOWN": "simt"}, {"PCC_HEAD": "simt", "PCC_CONV": "simt"},
                                  {"PCC_HEAD": "t2"}, {"PCC_HEAD": "q4"}, {"PCC_KMAP": "hash"},
                                  {"PCC_CONV": "tc1"}, {"PCC_HEAD": "t3g3"}, {"PCC_HEAD": "t1"},
-                                 {"PCC_KMAP": "derive27"}])
+                                 {"PCC_KMAP": "derive27"}, {"PCC_HEAD": "t3"}])
 def test_alternate_kernels_bit_exact(pcc, env):
     import os
     import subprocess

@@ -184,6 +184,39 @@ def test_saturating_logit_requant(pcc, ctx, sat_frac, C):
         pcc.pcc_model_destroy(m)
 
 
+@pytest.mark.parametrize("bmax", [500_000, 3_000_000])
+@pytest.mark.parametrize("C", [8, 32])
+def test_bias_fold_boundary(pcc, ctx, bmax, C):
+    """head4_tc.cu carries b1 / b2 as a second MMA slab of base-127 digits, exact for |b| <=
+    500000 (31 * 127 * 127 + 126); beyond it the library runs head3 (TMEM-seeded bias).
+    Biases drawn up to bmax, with the extremes +-bmax present, on both sides of the bound."""
+    model = I.make_model(C=C, H=C, seed=11, min_depth=9, max_depth=14)
+    rng = np.random.default_rng(bmax + C)
+    for h in [s.head for s in model.shallow.values()] + [dp.head for dp in model.deep]:
+        h.b1 = rng.integers(-bmax, bmax + 1, size=h.b1.shape).astype(np.int32)
+        h.b2 = rng.integers(-bmax, bmax + 1, size=h.b2.shape).astype(np.int32)
+        h.b1.flat[0], h.b2.flat[0], h.b2.flat[-1] = bmax, -bmax, bmax
+    mb = model.to_bytes()
+    om = O.Model(mb)
+    pts = I.make_frame(I.CFG1, 2)
+    D = O.Dump()
+    O.encode(om, pts, 12, D)
+    m = pcc.pcc_model_load(mb, 0)
+    try:
+        pcc.pcc_ctx_set_debug(ctx, True)
+        try:
+            gpu_encode(pcc, ctx, m, [pts], 12)
+            assert _compare_dumps(pcc, ctx, D, 12) > 30
+            gpu_decode(pcc, ctx, m, [O.encode(om, pts, 12)], len(pts))
+            for d in range(4, 12):
+                check_decoder_rows(pcc, ctx, D, d, model)
+        finally:
+            pcc.pcc_ctx_set_debug(ctx, False)
+        _check_frames(pcc, ctx, m, om, [pts, I.make_frame(I.CFG2, 1)], 12)
+    finally:
+        pcc.pcc_model_destroy(m)
+
+
 # ---------------------------------------------------------------------------------------
 # decoder rows at C = 32 (the bench's model width)
 # ---------------------------------------------------------------------------------------
