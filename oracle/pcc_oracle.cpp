@@ -559,12 +559,12 @@ void cdf_quantize(const int32_t* z, const RQ& rql, const std::vector<uint32_t>& 
 
 // ---- rANS (reading O9/O10/Q23/Q24) ---------------------------------------------
 // 32-bit state, L = 2^16, 16-bit words, M = 2^16.  Symbol j of a segment of n goes to
-// lane j mod K at step j / K with K = clamp(ceil(n/512), 1, 32) (segments of 16384 symbols:
-// at most 512 sequential steps per lane, reading Q24).
+// lane j mod K at step j / K with K = clamp(ceil(n/512), 1, 8) (segments of 4096 symbols:
+// at most 512 sequential steps per lane, reading Q24').
 int lanes_for(size_t n) {
   size_t k = (n + 511) / 512;
   if (k < 1) k = 1;
-  if (k > 32) k = 32;
+  if (k > 8) k = 8;
   return int(k);
 }
 
@@ -817,11 +817,11 @@ struct Coder {
 };
 
 // ---- Container (reading O11) ------------------------------------------------------
-// header (24 B): "PCC1" | u16 version=1 | u8 L | u8 R | u8 n_deep | u8 flags=0 |
+// header (24 B): "PCC1" | u16 version=2 (reading Q24': 4096-symbol segments) | u8 L | u8 R | u8 n_deep | u8 flags=0 |
 //                u16 raw_bytes | u32 N_L | u64 model_hash
 // u32 level_bytes[L-R]; raw prefix X_0..X_{R-1} (raw_bytes, zero-padded to 4);
 // level payloads d = R..L-1 (each a sequence of 4-byte-aligned rANS segments).
-constexpr size_t SEG = 16384;
+constexpr size_t SEG = 4096;
 
 void check_depth(const Model& m, int L) {
   if (L < m.R + 1 + m.n_deep || L < m.min_depth || L > m.max_depth || L > 21) throw Fail{UNSUPPORTED_DEPTH};
@@ -861,7 +861,7 @@ std::vector<uint8_t> encode(const Model& m, const int32_t* xyz, size_t n, int L,
   }
   std::vector<uint8_t> bs;
   bs.insert(bs.end(), {'P', 'C', 'C', '1'});
-  put_u16(bs, 1);
+  put_u16(bs, 2);
   bs.push_back(uint8_t(L));
   bs.push_back(uint8_t(R));
   bs.push_back(uint8_t(m.n_deep));
@@ -885,7 +885,7 @@ std::vector<uint8_t> encode(const Model& m, const int32_t* xyz, size_t n, int L,
 std::vector<uint64_t> decode(const Model& m, const uint8_t* bs, size_t len, int& L_out, Dump* Dp) {
   if (len < 24) throw Fail{TRUNCATED};
   if (std::memcmp(bs, "PCC1", 4) != 0) throw Fail{BAD_MAGIC};
-  if ((uint32_t(bs[4]) | uint32_t(bs[5]) << 8) != 1u) throw Fail{VERSION};
+  if ((uint32_t(bs[4]) | uint32_t(bs[5]) << 8) != 2u) throw Fail{VERSION};
   const int L = bs[6], R = bs[7], nd = bs[8];
   const size_t raw = uint32_t(bs[10]) | uint32_t(bs[11]) << 8;
   const uint32_t NL = get_u32(bs + 12);

@@ -14,8 +14,8 @@
 namespace pcc {
 
 constexpr int NCODE = 255;     // occupancy classes
-constexpr int SEG_SYMS = 16384; // rANS segment length (reading Q24: <= 512 steps per lane)
-constexpr int MAX_LANES = 32;
+constexpr int SEG_SYMS = 4096;  // rANS segment length (reading Q24': <= 512 steps per lane, K <= 8)
+constexpr int MAX_LANES = 8;
 constexpr int MAX_DEPTH = 21;   // 63-bit Morton key cap
 
 // Device error flags (atomicOr'ed by kernels, read at sync points).
@@ -290,7 +290,7 @@ struct DecSeg {
 // LUT[(mu - l_i) >> 2] and C_i = i + floor(E_i * 65281 / S) where its search needs them.
 constexpr int DROW_BYTES = 112, DROW_A = 80, DROW_U16 = DROW_BYTES / 2;
 void rans_decode(pcc_ctx c, const DecSeg* d_segs, int nseg, const uint8_t* bs, const uint16_t* rows, int H,
-                 const DHead& head, const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes, size_t nsym);
+                 const DHead& head, const uint32_t* lut, uint8_t* X, uint32_t* err, int max_lanes, size_t nsym, size_t nstates);
 
 // ---- modelgen.cu ----
 bool model_config_valid(const pcc_model_config& c);

@@ -170,7 +170,7 @@ bool bias_digits(const std::vector<int32_t>& b, std::vector<int8_t>& D) {
 
 inline int lanes_for(uint32_t n) {
   uint32_t k = (n + 511u) / 512u;
-  return int(k < 1u ? 1u : (k > 32u ? 32u : k));
+  return int(k < 1u ? 1u : (k > 8u ? 8u : k));
 }
 
 // ============================================================================
@@ -639,7 +639,7 @@ __global__ void k_pack_write(const PackItem* __restrict__ items, int n, const ui
     const uint32_t NL = foff[L * (B + 1) + f + 1] - foff[L * (B + 1) + f];
     if (lane == 0) {
       o[0] = 'P'; o[1] = 'C'; o[2] = 'C'; o[3] = '1';
-      o[4] = 1; o[5] = 0;
+      o[4] = 2; o[5] = 0;  // container version 2: 4096-symbol segments (reading Q24')
       o[6] = uint8_t(L); o[7] = uint8_t(R); o[8] = uint8_t(n_deep); o[9] = uint8_t(flags);
       o[10] = uint8_t(raw); o[11] = uint8_t(raw >> 8);
       for (int b = 0; b < 4; ++b) o[12 + b] = uint8_t(NL >> (8 * b));
@@ -901,7 +901,7 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
     const uint8_t* h = hh.data() + size_t(f) * HB;
     if (len[f] < 24) throw Error{PCC_ERR_TRUNCATED};
     if (std::memcmp(h, "PCC1", 4) != 0) throw Error{PCC_ERR_BAD_MAGIC};
-    if ((h[4] | h[5] << 8) != 1) throw Error{PCC_ERR_VERSION};
+    if ((h[4] | h[5] << 8) != 2) throw Error{PCC_ERR_VERSION};
     Hdr& x = hd[f];
     x.L = h[6]; x.R = h[7]; x.nd = h[8];
     x.raw = uint32_t(h[10]) | uint32_t(h[11]) << 8;
@@ -1043,9 +1043,13 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
     PCC_CUDA(cudaMemcpyAsync(d_segs, seg_ring + seg_ring_used, seg_bytes, cudaMemcpyHostToDevice, s));
     seg_ring_used += (seg_bytes + 255) & ~size_t(255);
     int kmax = 1;
-    for (const DecSeg& sg : segs) kmax = std::max(kmax, lanes_for(sg.n));
+    size_t nstates = 0;
+    for (const DecSeg& sg : segs) {
+      kmax = std::max(kmax, lanes_for(sg.n));
+      nstates += size_t(lanes_for(sg.n));
+    }
     rans_decode(c, d_segs, int(segs.size()), d_bs, cdf, m->H, net.head_of(d), m->lut,
-                static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d], err, kmax, nd);
+                static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d], err, kmax, nd, nstates);
     if (c->debug) dbg_copy(c, nm("code", d), static_cast<uint8_t*>(c->bufs.at("code").p) + o.nb[d], nd);
     expand_level(c, d, B, o, uint32_t(std::min<uint64_t>(NLtot, 0xffffffffu)), err);
   }

@@ -334,7 +334,7 @@ def test_zero_model_and_max_depth(pcc, ctx):
 
 
 def test_large_level_multi_segment(pcc, ctx):
-    """A level with > 16384 nodes spans several rANS segments (reading Q24)."""
+    """A level with > 4096 nodes spans several rANS segments (reading Q24')."""
     mb, om = model_pair(8, max_depth=12)
     m = gpu_model(pcc, mb)
     pts = I.random_cloud(150000, 12, 21)
@@ -474,7 +474,8 @@ print("ALT-OK")
 @pytest.mark.parametrize("env", [{"PCC_UP": "simt", "PCC_DOWN": "simt"}, {"PCC_HEAD": "simt", "PCC_CONV": "simt"},
                                  {"PCC_HEAD": "t2"}, {"PCC_HEAD": "q4"}, {"PCC_KMAP": "hash"},
                                  {"PCC_CONV": "tc1"}, {"PCC_HEAD": "t3g3"}, {"PCC_HEAD": "t1"},
-                                 {"PCC_KMAP": "derive27"}, {"PCC_HEAD": "t3"}])
+                                 {"PCC_KMAP": "derive27"}, {"PCC_HEAD": "t3"}, {"PCC_RDEC": "t2"}, {"PCC_RDEC": "t4"},
+                                 {"PCC_RDEC": "old"}])
 def test_alternate_kernels_bit_exact(pcc, env):
     import os
     import subprocess

@@ -122,7 +122,7 @@ def test_rans_round_trip_and_length(n, peaky):
     data = O.rans_encode(c, f)
     out, used = O.rans_decode(data, pmf)
     assert used == len(data) and np.array_equal(out, sym)
-    K = min(32, max(1, -(-n // 512)))
+    K = min(8, max(1, -(-n // 512)))
     ideal_bits = float(np.sum(np.log2(65536.0 / f)))
     payload_bits = 8 * (len(data) - 4 - 4 * K)       # words (+pad), excluding W and states
     # upper: each lane's flush costs its 32-bit final state (counted separately) and

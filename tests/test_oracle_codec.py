@@ -60,8 +60,8 @@ def _payload_bits(level_bytes, N):
     """Bits of rANS words in a level payload (segment headers/states excluded) and lane count."""
     bits, lanes, pos, left = 0, 0, 0, N
     while left > 0:
-        n = min(16384, left)
-        K = min(32, max(1, -(-n // 512)))
+        n = min(4096, left)
+        K = min(8, max(1, -(-n // 512)))
         W = struct.unpack_from("<I", level_bytes, pos)[0]
         bits += 16 * W
         lanes += K
@@ -195,7 +195,7 @@ def test_errors(model):
     assert st(lambda: O.encode(model, pts, 8)) == "UNSUPPORTED_DEPTH"
     assert st(lambda: O.encode(model, pts, 13)) == "UNSUPPORTED_DEPTH"
     assert st(lambda: O.decode(model, b"XCC1" + bs[4:])) == "BAD_MAGIC"
-    assert st(lambda: O.decode(model, bs[:4] + b"\x02\x00" + bs[6:])) == "VERSION"
+    assert st(lambda: O.decode(model, bs[:4] + b"\x01\x00" + bs[6:])) == "VERSION"
     other = O.Model(I.make_model(C=8, H=8, seed=6, min_depth=9, max_depth=12).to_bytes())
     assert st(lambda: O.decode(other, bs)) == "MODEL_MISMATCH"
     assert st(lambda: O.decode(model, bs[:len(bs) - 7])) in ("TRUNCATED", "CORRUPT")
