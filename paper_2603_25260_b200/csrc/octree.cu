@@ -32,47 +32,59 @@ __device__ __forceinline__ uint32_t compact3(uint64_t x) {
 }
 
 // ---- a1: Morton keys (x is the MSB of each bit triple, reading O1/Q25) -------------
-__global__ void k_morton(const int32_t* __restrict__ xyz, size_t n, const uint64_t* __restrict__ offs, int B, int L,
-                         uint64_t* __restrict__ keys, uint32_t* __restrict__ flags, uint32_t* __restrict__ err) {
-  size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int32_t x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+// a1 front end in one pass (r2): Morton keys, the consecutive-duplicate drop and the
+// compaction together.  Grid (tiles, frames), MD_V points per thread at stride MD_T: each
+// CTA counts its kept keys (warp ballots + one shared-memory atomic per warp), reserves its
+// range of the frame's output with ONE global atomic, and writes the kept keys from
+// registers.  The kept keys of a frame land at out[offs[f] ..  offs[f] + kept[f]) in an
+// arbitrary order: the radix sort below orders them (a sort is a function of the multiset),
+// so the result is deterministic.
+constexpr int MD_T = 256, MD_V = 16, MD_TILE = MD_T * MD_V;
+__global__ void __launch_bounds__(MD_T) k_morton_dedup(const int32_t* __restrict__ xyz, const uint64_t* __restrict__ offs,
+                                                       int B, int L, uint64_t* __restrict__ out,
+                                                       uint32_t* __restrict__ kept, uint32_t* __restrict__ err) {
+  __shared__ uint32_t s_cnt, s_base;
+  const int f = blockIdx.y;
+  const uint64_t a = offs[f];
+  const uint32_t nf = uint32_t(offs[f + 1] - a);
+  const uint32_t c0 = blockIdx.x * MD_TILE;
+  if (c0 >= nf) return;  // whole CTA
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
   const int32_t lim = 1 << L;
-  if (x < 0 || y < 0 || z < 0 || x >= lim || y >= lim || z >= lim) {
-    atomicOr(err, EF_RANGE);
-    keys[i] = 0;
-    flags[i] = 1u;
-    return;
+  const uint64_t fb = B > 1 ? uint64_t(f) << (3 * L) : 0ull;
+  uint64_t kv[MD_V];
+  uint32_t keepm = 0, woff[MD_V];
+#pragma unroll
+  for (int v = 0; v < MD_V; ++v) {
+    const uint32_t i = c0 + uint32_t(v) * MD_T + threadIdx.x;  // frame-local point index
+    bool keep = false;
+    kv[v] = 0;
+    if (i < nf) {
+      const int32_t* p = xyz + 3 * (a + i);
+      const int32_t x = p[0], y = p[1], z = p[2];
+      if (x < 0 || y < 0 || z < 0 || x >= lim || y >= lim || z >= lim) {
+        atomicOr(err, EF_RANGE);
+      } else {
+        keep = i == 0 || p[-3] != x || p[-2] != y || p[-1] != z;
+        kv[v] = fb | spread3(uint32_t(x)) << 2 | spread3(uint32_t(y)) << 1 | spread3(uint32_t(z));
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    uint32_t wb = 0;
+    if (lane == 0 && m) wb = atomicAdd(&s_cnt, uint32_t(__popc(m)));
+    wb = __shfl_sync(0xffffffffu, wb, 0);
+    woff[v] = wb + __popc(m & ((1u << lane) - 1u));
+    keepm |= keep ? (1u << v) : 0u;
   }
-  // frame id: largest f with offs[f] <= i
-  int lo = 0, hi = B - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (offs[mid] <= i) lo = mid; else hi = mid - 1;
-  }
-  uint64_t m = spread3(uint32_t(x)) << 2 | spread3(uint32_t(y)) << 1 | spread3(uint32_t(z));
-  keys[i] = (B > 1 ? (uint64_t(lo) << (3 * L)) : 0ull) | m;
-  // keep flag: the first point of a frame, or a point whose voxel differs from the previous
-  // point's (consecutive duplicates in input order, e.g. adjacent azimuths of one beam, are
-  // dropped before the sort; the sort + unique below still removes every other duplicate)
-  bool keep = offs[lo] == i;
-  if (!keep) {
-    const int32_t px = xyz[3 * i - 3], py = xyz[3 * i - 2], pz = xyz[3 * i - 1];
-    keep = px != x || py != y || pz != z;
-  }
-  flags[i] = keep ? 1u : 0u;
-}
-
-// compaction of the kept keys (exclusive scan pos of the flags) and the new frame offsets
-__global__ void k_dedup_compact(const uint64_t* __restrict__ in, size_t n, const uint32_t* __restrict__ flags,
-                                const uint32_t* __restrict__ pos, uint64_t* __restrict__ out) {
-  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n && flags[i]) out[pos[i]] = in[i];
-}
-__global__ void k_dedup_offs(const uint64_t* __restrict__ offs, int B, const uint32_t* __restrict__ pos,
-                             uint64_t* __restrict__ noffs) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f <= B) noffs[f] = pos[offs[f]];
+  __syncthreads();
+  if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(&kept[f], s_cnt) : 0u;
+  __syncthreads();
+  uint64_t* o = out + a + s_base;
+#pragma unroll
+  for (int v = 0; v < MD_V; ++v)
+    if (keepm >> v & 1u) o[woff[v]] = kv[v];
 }
 
 // ---- radix sort (LSD, 8- or 9-bit digits, stable per pass, frame-segmented) ----------
@@ -89,7 +101,7 @@ struct __align__(16) RsTile {  // tile g -> its frame's key range and histogram 
 };
 // once per sort: one thread per tile
 __global__ void k_rs_tiles(const uint32_t* __restrict__ tp, const uint64_t* __restrict__ offs, int B, uint32_t ntiles,
-                           RsTile* __restrict__ tiles) {
+                           RsTile* __restrict__ tiles, const uint64_t* __restrict__ in_offs, RsTile* __restrict__ tiles_in) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ntiles) return;
   int lo = 0, hi = B - 1;  // frame: largest f < B with tp[f] <= g
@@ -103,6 +115,9 @@ __global__ void k_rs_tiles(const uint32_t* __restrict__ tp, const uint64_t* __re
   t.start = uint32_t(offs[lo]) + (g - t.T0) * uint32_t(RS_TILE);
   t.count = min(uint32_t(RS_TILE), uint32_t(offs[lo + 1]) - t.start);
   tiles[g] = t;
+  // the first pass reads frame f's keys where k_morton_dedup left them (from in_offs[f])
+  t.start = uint32_t(in_offs[lo]) + (g - t.T0) * uint32_t(RS_TILE);
+  tiles_in[g] = t;
 }
 
 template <int DB>
@@ -389,50 +404,57 @@ void build_octree(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int B, in
   cudaStream_t s = c->stream;
   // device copy of frame offsets
   uint64_t* d_offs = wsT<uint64_t>(c, "oct_offs", B + 1);
-  // pinned staging: offs (u64) then the sort's per-frame first tiles (u32)
-  uint64_t* h = static_cast<uint64_t*>(pinned(c, (B + 1) * (sizeof(uint64_t) + sizeof(uint32_t))));
-  for (int f = 0; f <= B; ++f) h[f] = offs[f];
-  PCC_CUDA(cudaMemcpyAsync(d_offs, h, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  // pinned staging, one block (no reallocation while a copy from it is pending): input offs
+  // (u64), kept counts (u32), kept offsets (u64), the sort's per-frame first tiles (u32)
+  const size_t B1 = size_t(B) + 1, B2 = (B1 + 2) & ~size_t(1);  // hk[B] = the error flags
+  uint64_t* h_in = static_cast<uint64_t*>(pinned(c, B1 * 8 + B2 * 4 + B1 * 8 + B1 * 4));
+  uint32_t* hk = reinterpret_cast<uint32_t*>(h_in + B1);
+  uint64_t* h = reinterpret_cast<uint64_t*>(hk + B2);
+  for (int f = 0; f <= B; ++f) h_in[f] = offs[f];
+  PCC_CUDA(cudaMemcpyAsync(d_offs, h_in, B1 * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   uint32_t* err = wsT<uint32_t>(c, "err", 4);
   PCC_CUDA(cudaMemsetAsync(err, 0, 4 * sizeof(uint32_t), s));
 
   uint64_t* ka = wsT<uint64_t>(c, "sort_a", n_in);
   uint64_t* kb = wsT<uint64_t>(c, "sort_b", n_in);
-  uint32_t* flags = wsT<uint32_t>(c, "dd_flags", n_in);
-  uint32_t* pos = wsT<uint32_t>(c, "dd_pos", n_in + 1);
+  uint32_t* kept = wsT<uint32_t>(c, "dd_kept", B);
   uint64_t* d_noffs = wsT<uint64_t>(c, "dd_offs", B + 1);
+  PCC_CUDA(cudaMemsetAsync(kept, 0, B * sizeof(uint32_t), s));
   {
-    Prof p(c, "morton", n_in * 24);
-    k_morton<<<cdiv(n_in, 256), 256, 0, s>>>(d_xyz, n_in, d_offs, B, L, ka, flags, err);
+    // Morton keys + consecutive-duplicate drop + compaction in one pass: LiDAR frames arrive
+    // in scan order, where neighbouring returns of one beam often share a voxel (cfg2: 131k
+    // points -> 61k kept, 56k unique)
+    Prof p(c, "morton", n_in * 12 + n_in * 8);
+    size_t maxf = 0;
+    for (int f = 0; f < B; ++f) maxf = std::max<size_t>(maxf, offs[f + 1] - offs[f]);
+    k_morton_dedup<<<dim3(cdiv(std::max<size_t>(maxf, 1), MD_TILE), B), MD_T, 0, s>>>(d_xyz, d_offs, B, L, ka, kept,
+                                                                                     err);
     launched(c);
   }
-  // drop consecutive duplicates (input order) before the sort: LiDAR frames arrive in scan
-  // order, where neighbouring returns of one beam often share a voxel (cfg2: 131k points ->
-  // 61k kept, 56k unique); the frames stay contiguous, their offsets shrink
-  scan_u32(c, flags, pos, n_in);
-  {
-    Prof p(c, "morton", n_in * 16);
-    k_dedup_compact<<<cdiv(n_in, 256), 256, 0, s>>>(ka, n_in, flags, pos, kb);
-    k_dedup_offs<<<cdiv(B + 1, 256), 256, 0, s>>>(d_offs, B, pos, d_noffs);
-    launched(c, 2);
-  }
-  std::swap(ka, kb);
-  PCC_CUDA(cudaMemcpyAsync(h, d_noffs, (B + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  PCC_CUDA(cudaMemcpyAsync(hk, kept, B * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  PCC_CUDA(cudaMemcpyAsync(hk + B, err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   PCC_CUDA(cudaStreamSynchronize(s));
+  if (hk[B] & EF_RANGE) throw Error{PCC_ERR_RANGE};  // out-of-range points are not kept
+  // kept offsets (contiguous, what the sort writes) on the host and the device
+  h[0] = 0;
+  for (int f = 0; f < B; ++f) h[f + 1] = h[f] + hk[f];
   const size_t n = h[B];
+  PCC_CUDA(cudaMemcpyAsync(d_noffs, h, (B + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  const uint64_t* d_in_offs = d_offs;
   d_offs = d_noffs;
 
   // frame-aligned tiles: tp[f] = first tile of frame f (host copy of the kept offsets)
-  uint32_t* htp = reinterpret_cast<uint32_t*>(h + (B + 1));
+  uint32_t* htp = reinterpret_cast<uint32_t*>(h + (B + 1));  // inside the pinned block above
   htp[0] = 0;
   for (int f = 0; f < B; ++f) htp[f + 1] = htp[f] + cdiv(h[f + 1] - h[f], RS_TILE);
   const uint32_t ntiles = htp[B];
   uint32_t* d_tp = wsT<uint32_t>(c, "rs_tp", B + 1);
   PCC_CUDA(cudaMemcpyAsync(d_tp, htp, (B + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
   RsTile* tiles = wsT<RsTile>(c, "rs_tiles", ntiles);
+  RsTile* tiles_in = wsT<RsTile>(c, "rs_tiles_in", ntiles);
   {
     Prof p(c, "sort", 0);
-    k_rs_tiles<<<cdiv(ntiles, 256), 256, 0, s>>>(d_tp, d_offs, B, ntiles, tiles);
+    k_rs_tiles<<<cdiv(ntiles, 256), 256, 0, s>>>(d_tp, d_offs, B, ntiles, tiles, d_in_offs, tiles_in);
     launched(c);
   }
   // 3L Morton bits in 8- or 9-bit digits, whichever needs fewer passes
@@ -446,15 +468,17 @@ void build_octree(pcc_ctx c, const int32_t* d_xyz, const size_t* offs, int B, in
   for (int sh = 0; sh < bits; sh += DB) {
     {
       Prof p(c, "sort", n * 8);
-      if (DB == 9) k_rs_hist<9><<<ntiles, RS_T, 0, s>>>(ka, sh, tiles, hist);
-      else k_rs_hist<8><<<ntiles, RS_T, 0, s>>>(ka, sh, tiles, hist);
+      const RsTile* tl = sh == 0 ? tiles_in : tiles;
+      if (DB == 9) k_rs_hist<9><<<ntiles, RS_T, 0, s>>>(ka, sh, tl, hist);
+      else k_rs_hist<8><<<ntiles, RS_T, 0, s>>>(ka, sh, tl, hist);
       launched(c);
     }
     scan_u32(c, hist, hist, (size_t(1) << DB) * ntiles);
     {
       Prof p(c, "sort", n * 16);
-      if (DB == 9) k_rs_scatter<9><<<ntiles, RS_T, 0, s>>>(ka, kb, sh, tiles, hist);
-      else k_rs_scatter<8><<<ntiles, RS_T, 0, s>>>(ka, kb, sh, tiles, hist);
+      const RsTile* tl = sh == 0 ? tiles_in : tiles;
+      if (DB == 9) k_rs_scatter<9><<<ntiles, RS_T, 0, s>>>(ka, kb, sh, tl, hist);
+      else k_rs_scatter<8><<<ntiles, RS_T, 0, s>>>(ka, kb, sh, tl, hist);
       launched(c);
     }
     std::swap(ka, kb);

@@ -15,27 +15,31 @@ __device__ __forceinline__ int lanes_for(uint32_t n) {
   return int(k < 1u ? 1u : (k > 8u ? 8u : k));
 }
 
+// Lane groups of MAX_LANES = 8: a warp encodes 4 segments side by side (reading Q24': K <= 8).
 __global__ void __launch_bounds__(128) k_rans_enc(const EncSeg* __restrict__ segs, int nseg, const uint32_t* __restrict__ cf,
                                                   uint16_t* __restrict__ words, uint32_t* __restrict__ seg_W,
                                                   uint32_t* __restrict__ seg_state) {
-  const int gw = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  if (gw >= nseg) return;
-  const EncSeg sg = segs[gw];
+  constexpr int G = MAX_LANES;
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), gb = lane - gl;
+  const int gw = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G) + (lane / G);
+  if (int((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G) >= nseg) return;  // whole warp idle
+  const bool seg = gw < nseg;
+  const EncSeg sg = seg ? segs[gw] : EncSeg{0, 0};
   const uint32_t n = sg.n;
-  const int K = lanes_for(n);
-  const uint32_t steps = (n + uint32_t(K) - 1u) / uint32_t(K);
+  const int K = seg ? lanes_for(n) : 1;
+  const uint32_t steps = seg ? (n + uint32_t(K) - 1u) / uint32_t(K) : 0u;
+  const uint32_t steps_max = __reduce_max_sync(0xffffffffu, steps);
   uint32_t x = 1u << 16;
   uint32_t cnt = 0;
   uint16_t* end = words + sg.node + n;
-  const unsigned above = ~((2u << lane) - 1u);  // lanes with a higher index
-  for (uint32_t s = steps; s-- > 0;) {
-    const uint32_t j = s * uint32_t(K) + uint32_t(lane);
-    const bool act = lane < K && j < n;
+  const unsigned above = ~((2u << gl) - 1u) & 0xffu;  // lanes of the group with a higher index
+  for (uint32_t s = steps_max; s-- > 0;) {
+    const uint32_t j = s * uint32_t(K) + uint32_t(gl);
+    const bool act = s < steps && gl < K && j < n;
     const uint32_t v = act ? cf[sg.node + j] : 0u;
     const uint32_t c = v & 0xffffu, f = v >> 16;
     const bool emit = act && x >= (f << 16);
-    const unsigned m = __ballot_sync(0xffffffffu, emit);
+    const unsigned m = (__ballot_sync(0xffffffffu, emit) >> gb) & 0xffu;
     if (emit) {
       end[-1 - int(cnt + __popc(m & above))] = uint16_t(x & 0xffffu);
       x >>= 16;
@@ -43,8 +47,8 @@ __global__ void __launch_bounds__(128) k_rans_enc(const EncSeg* __restrict__ seg
     cnt += __popc(m);
     if (act) x = ((x / f) << 16) + (x % f) + c;
   }
-  if (lane == 0) seg_W[gw] = cnt;
-  if (lane < K) seg_state[size_t(gw) * 32 + lane] = x;
+  if (seg && gl == 0) seg_W[gw] = cnt;
+  if (seg && gl < K) seg_state[size_t(gw) * 32 + gl] = x;
 }
 
 __device__ __forceinline__ uint32_t ld_u32(const uint8_t* p) {
@@ -606,7 +610,7 @@ __global__ void __launch_bounds__(32 * DEC_WPC) k_rans_dec_t(const DecSeg* __res
 void rans_encode(pcc_ctx c, const EncSeg* d_segs, int nseg, const uint32_t* cf, uint16_t* words, uint32_t* seg_W,
                  uint32_t* seg_state) {
   if (nseg == 0) return;
-  const unsigned grid = unsigned((size_t(nseg) * 32 + 127) / 128);
+  const unsigned grid = unsigned((size_t(nseg) * MAX_LANES + 127) / 128);
   Prof p(c, "rans_enc", 0);
   k_rans_enc<<<grid, 128, 0, c->stream>>>(d_segs, nseg, cf, words, seg_W, seg_state);
   launched(c);
