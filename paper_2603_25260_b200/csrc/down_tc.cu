@@ -31,13 +31,16 @@ __device__ __forceinline__ void bar_group(int id) { asm volatile("bar.sync %0, 1
 
 // smem: per group an A tile [128 x 256] (8 canonical slabs of 4 KB); B = 8 slabs [32 x 32];
 // mbarriers + TMEM holder
-constexpr int SM_A = 0, SM_B = DG * 32768, SM_MBAR = SM_B + 8192, SM_END = SM_MBAR + 8 * DG + 16;
+constexpr int SM_A = 0, SM_B = DG * 32768, SM_MBAR = SM_B + 8192, SM_E = SM_MBAR + 128, SM_END = SM_E + NCODE * 32;
 
-template <bool SIGNED>
+// EMB: the child rows are the embedding g = E[X_c - 1] of the children's codes (Eq.4, the
+// first K2S2 step of a deep level, reading Q5): gathered straight from the 255 x 32 table
+// instead of a materialised embedded level.
+template <bool SIGNED, bool EMB>
 __global__ void __launch_bounds__(DNT, 1) k_down_tc(const int8_t* __restrict__ g, const uint8_t* __restrict__ Xp,
                                                     const uint32_t* __restrict__ cs, uint32_t np,
                                                     const int8_t* __restrict__ W, const int32_t* __restrict__ bias,
-                                                    RQ rq, int8_t* __restrict__ out) {
+                                                    RQ rq, int8_t* __restrict__ out, const uint8_t* __restrict__ Xc) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const int t = threadIdx.x, grp = t >> 7, r = t & 127;  // group, parent row of the tile (= TMEM lane)
   uint8_t* sA = sm + SM_A + grp * 32768;
@@ -51,6 +54,8 @@ __global__ void __launch_bounds__(DNT, 1) k_down_tc(const int8_t* __restrict__ g
         reinterpret_cast<const uint4*>(W)[k];
   }
   for (int k = t; k < DG * 32768 / 16; k += DNT) reinterpret_cast<uint4*>(sm + SM_A)[k] = make_uint4(0u, 0u, 0u, 0u);
+  if (EMB)  // the embedding table: every child row of the step is one of its 255 rows
+    for (int k = t; k < NCODE * 2; k += DNT) reinterpret_cast<uint4*>(sm + SM_E)[k] = reinterpret_cast<const uint4*>(g)[k];
   if (t < 32) tc::tmem_alloc<32 * DG>(thold);
   if (r == 0) tc::mbar_init(mbar, 1);
   if (blockIdx.x == 0 && t < 8) reinterpret_cast<uint32_t*>(out + size_t(np) * 32)[t] = 0u;  // zero row
@@ -70,23 +75,40 @@ __global__ void __launch_bounds__(DNT, 1) k_down_tc(const int8_t* __restrict__ g
   const uint32_t stride = gridDim.x * DG;
   uint32_t tile = blockIdx.x * DG + grp;
   uint32_t phase = 0;
-  auto load = [&](uint32_t tl, uint32_t& xx, uint32_t& jj) {  // code and child start of row r of tile tl
+  // code and child start of row r of tile tl; EMB: the children's codes, packed (loaded
+  // two tiles ahead with the rest, so the gather never waits on them)
+  auto load = [&](uint32_t tl, uint32_t& xx, uint32_t& jj, uint64_t& cw) {
     const uint32_t p = tl * 128 + r;
-    xx = 0u, jj = 0u;
-    if (tl < ntiles && p < np) xx = Xp[p], jj = cs[p];
+    xx = 0u, jj = 0u, cw = 0ull;
+    if (tl < ntiles && p < np) {
+      xx = Xp[p], jj = cs[p];
+      if (EMB) {
+        const int nc = __popc(xx);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < nc) cw |= uint64_t(Xc[jj + k]) << (8 * k);
+      }
+    }
   };
-  auto gather = [&](uint32_t xx, uint32_t jj) {  // child rows into their K-slots of row r
-    for (uint32_t m = xx; m; m &= m - 1u, ++jj) {
+  auto gather = [&](uint32_t xx, uint32_t jj, uint64_t cw) {  // child rows into their K-slots of row r
+    for (uint32_t m = xx; m; m &= m - 1u, ++jj, cw >>= 8) {
       const uint32_t c = __ffs(m) - 1;
-      cp16(sA + c * 4096 + tc::kmaj_off(r, 0), g + size_t(jj) * 32);
-      cp16(sA + c * 4096 + tc::kmaj_off(r, 16), g + size_t(jj) * 32 + 16);
+      if (EMB) {  // from the shared-memory table (a 8 KB hot set would serialise in L2)
+        const uint4* src = reinterpret_cast<const uint4*>(sm + SM_E + (uint32_t(cw & 0xffu) - 1u) * 32u);
+        *reinterpret_cast<uint4*>(sA + c * 4096 + tc::kmaj_off(r, 0)) = src[0];
+        *reinterpret_cast<uint4*>(sA + c * 4096 + tc::kmaj_off(r, 16)) = src[1];
+      } else {
+        cp16(sA + c * 4096 + tc::kmaj_off(r, 0), g + size_t(jj) * 32);
+        cp16(sA + c * 4096 + tc::kmaj_off(r, 16), g + size_t(jj) * 32 + 16);
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
   uint32_t x, j0, xn, jn;
-  load(tile, x, j0);
-  load(tile + stride, xn, jn);
-  gather(x, j0);
+  uint64_t cw0, cwn;
+  load(tile, x, j0, cw0);
+  load(tile + stride, xn, jn, cwn);
+  gather(x, j0, cw0);
   for (; tile < ntiles; tile += stride) {
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     tc::fence_async_smem();
@@ -101,7 +123,8 @@ __global__ void __launch_bounds__(DNT, 1) k_down_tc(const int8_t* __restrict__ g
       tc::commit(mbar);
     }
     uint32_t x2, j2;
-    load(tile + 2 * stride, x2, j2);
+    uint64_t cw2;
+    load(tile + 2 * stride, x2, j2, cw2);
     tc::mbar_wait(mbar, phase);
     phase ^= 1u;
     tc::fence_after();
@@ -115,7 +138,7 @@ __global__ void __launch_bounds__(DNT, 1) k_down_tc(const int8_t* __restrict__ g
       *reinterpret_cast<uint4*>(sA + c * 4096 + tc::kmaj_off(r, 0)) = make_uint4(0u, 0u, 0u, 0u);
       *reinterpret_cast<uint4*>(sA + c * 4096 + tc::kmaj_off(r, 16)) = make_uint4(0u, 0u, 0u, 0u);
     }
-    gather(xn, jn);
+    gather(xn, jn, cwn);
     const uint32_t p = tile * 128 + r;
     if (p < np) {
       uint32_t o4[8];
@@ -135,7 +158,7 @@ __global__ void __launch_bounds__(DNT, 1) k_down_tc(const int8_t* __restrict__ g
       dst[1] = make_uint4(o4[4], o4[5], o4[6], o4[7]);
     }
     x = xn, j0 = jn;
-    xn = x2, jn = j2;
+    xn = x2, jn = j2, cwn = cw2;
   }
   __syncthreads();
   if (t < 32) tc::tmem_dealloc<32 * DG>(*thold);
@@ -144,17 +167,21 @@ __global__ void __launch_bounds__(DNT, 1) k_down_tc(const int8_t* __restrict__ g
 }  // namespace
 
 void down_tc(pcc_ctx c, const int8_t* g, const uint8_t* Xp, const uint32_t* cs_p, uint32_t np, const DDown& L,
-             int8_t* out) {
+             int8_t* out, const uint8_t* Xc) {
   constexpr int smem = SM_END;  // ~136 KB: one CTA (four tile groups) per SM
-  PCC_SMEM_ATTR(k_down_tc<true>, smem);
-  PCC_SMEM_ATTR(k_down_tc<false>, smem);
   const uint32_t ntiles = (np + 127) / 128;
   const unsigned grid = std::max(1u, std::min((ntiles + DG - 1) / DG, unsigned(c->sm_count)));
   Prof p(c, "down", size_t(np) * (1 + 4 + 32));
-  if (L.rq.fast_s)
-    k_down_tc<true><<<grid, DNT, smem, c->stream>>>(g, Xp, cs_p, np, L.W, L.b, L.rq, out);
-  else
-    k_down_tc<false><<<grid, DNT, smem, c->stream>>>(g, Xp, cs_p, np, L.W, L.b, L.rq, out);
+#define PCC_DOWN(SG, EM)                                                                                 \
+  do {                                                                                                   \
+    PCC_SMEM_ATTR((k_down_tc<SG, EM>), smem);                                                            \
+    k_down_tc<SG, EM><<<grid, DNT, smem, c->stream>>>(g, Xp, cs_p, np, L.W, L.b, L.rq, out, Xc);         \
+  } while (0)
+  if (L.rq.fast_s && Xc) PCC_DOWN(true, true);
+  else if (L.rq.fast_s) PCC_DOWN(true, false);
+  else if (Xc) PCC_DOWN(false, true);
+  else PCC_DOWN(false, false);
+#undef PCC_DOWN
   launched(c);
 }
 

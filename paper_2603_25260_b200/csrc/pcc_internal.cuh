@@ -260,7 +260,8 @@ void up_prune_tc(pcc_ctx c, const int8_t* S, const uint8_t* Xp, const uint32_t* 
 
 // ---- down_tc.cu (K2S2 downsampling as a block-diagonal tcgen05 product; C = 32) ----
 void down_tc(pcc_ctx c, const int8_t* g, const uint8_t* Xp, const uint32_t* cs_p, uint32_t np, const DDown& L,
-             int8_t* out);
+             int8_t* out,
+             const uint8_t* Xc = nullptr);
 
 // ---- conv_tc.cu (gather -> tcgen05 kind::i8 per kernel offset; C = 32) ----
 void conv3_tc(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,

@@ -553,17 +553,23 @@ struct Net {
     // Eq.4: G_D = Downsampling(X_{d-1}): embed on depth d-1 then K2S2 steps down to D
     int8_t* ga = buf<int8_t>(c, "t_ga", rows(d - 1) * C);
     int8_t* gb = buf<int8_t>(c, "t_gb", rows(d - 1) * C);
-    embed(c, dp.E, X(d - 1), o.N[d - 1], C, ga);
-    dbgF(nm("G", d, d - 1), ga, o.N[d - 1], C);
+    // C = 32: the tcgen05 kernel (down_tc.cu), whose first step gathers the embedding
+    // E[X_{d-1}] of the children directly (the embedded level is materialised only for a
+    // debug dump or when no down step follows); PCC_DOWN=simt selects the dp4a kernel
+    static const bool simt = [] {
+      const char* e = getenv("PCC_DOWN");
+      return e && std::string(e) == "simt";
+    }();
+    const bool fuse = C == 32 && !simt && j > 1 && !c->debug;
+    if (!fuse) {
+      embed(c, dp.E, X(d - 1), o.N[d - 1], C, ga);
+      dbgF(nm("G", d, d - 1), ga, o.N[d - 1], C);
+    }
     for (int s = 0; s < j - 1; ++s) {
       const int k = d - 1 - s;  // depth k -> k-1
-      // C = 32: the tcgen05 kernel (down_tc.cu); PCC_DOWN=simt selects the dp4a kernel
-      static const bool simt = [] {
-        const char* e = getenv("PCC_DOWN");
-        return e && std::string(e) == "simt";
-      }();
       if (C == 32 && !simt)
-        down_tc(c, ga, X(k - 1), cs() + o.nb[k - 1], o.N[k - 1], dp.down[s], gb);
+        down_tc(c, fuse && s == 0 ? dp.E : ga, X(k - 1), cs() + o.nb[k - 1], o.N[k - 1], dp.down[s], gb,
+                fuse && s == 0 ? X(d - 1) : nullptr);
       else
         down(c, ga, X(k - 1), cs() + o.nb[k - 1], o.N[k - 1], C, dp.down[s], gb);
       std::swap(ga, gb);
