@@ -299,9 +299,18 @@ __global__ void __launch_bounds__(CT) k_conv3_tc(const int8_t* __restrict__ in0,
 // runs.  Stage info (offset, accumulator, flags) is written by gather thread 0 before its
 // FULL arrival.  Tiles with no active offset still run one (zero) stage, so every tile
 // goes through TDONE.
-constexpr int WS_NS = 6;    // stages in the ring
+// Stages carry up to GS kernel offsets each (K = 32 GS SLABS), so the MMA warp pays one
+// FULL wait and one commit per GS offsets.
+template <int SLABS> struct WsCfg;
+template <> struct WsCfg<1> { static constexpr int NS = 6, GS = 3; };
+template <> struct WsCfg<2> { static constexpr int NS = 3, GS = 2; };
 constexpr int WS_NT = 288;  // 4 gather warps + 1 MMA warp + 4 epilogue warps
 enum : uint32_t { SI_ACC = 1u, SI_LAST = 2u, SI_END = 4u, SI_PROJ = 8u, SI_BUF1 = 16u };
+// info word: flags (bits 0..4), offsets in the stage (bits 5..6), offset u at bits 8 + 5u
+template <int SLABS, int SKIP>
+__host__ __device__ constexpr int ws_slabs() {  // 4 KB slabs per stage
+  return (WsCfg<SLABS>::GS * SLABS > (SKIP == 2 ? 2 : 0)) ? WsCfg<SLABS>::GS * SLABS : 2;
+}
 
 template <int SLABS, int SKIP>
 __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ in0, const int8_t* __restrict__ in1,
@@ -314,8 +323,8 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
   constexpr int ASLAB = CT * 32;
   constexpr int B_BYTES = 27 * SLABS * BSLAB;
   constexpr int P_BYTES = SKIP == 2 ? 2 * BSLAB : 0;
-  constexpr int NS = WS_NS;
-  constexpr int SS = (SKIP == 2) ? 2 : SLABS;  // slabs per stage (the projection stage has 2)
+  constexpr int NS = WsCfg<SLABS>::NS, GS = WsCfg<SLABS>::GS;
+  constexpr int SS = ws_slabs<SLABS, SKIP>();  // slabs per stage
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* sB = sm;
   uint8_t* sP = sm + B_BYTES;
@@ -380,16 +389,21 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
         }
         const uint32_t acc_t = tmem + 32u * b;
         const uint8_t* a = sA + st * SS * ASLAB;
-        const int dl = int(inf >> 8);
         if (inf & SI_PROJ) {
           tc::mma_i8(acc_t, tc::sdesc(tc::smem_u32(a)), tc::sdesc(tc::smem_u32(sP)), IDESC32, (inf & SI_ACC) ? 1u : 0u);
           tc::mma_i8(acc_t, tc::sdesc(tc::smem_u32(a + ASLAB)), tc::sdesc(tc::smem_u32(sP + BSLAB)), IDESC32, 1u);
         } else {
+          const int cnt = int((inf >> 5) & 3u);
 #pragma unroll
-          for (int sl = 0; sl < SLABS; ++sl)
-            tc::mma_i8(acc_t, tc::sdesc(tc::smem_u32(a + sl * ASLAB)),
-                       tc::sdesc(tc::smem_u32(sB + (dl * SLABS + sl) * BSLAB)), IDESC32,
-                       ((inf & SI_ACC) || sl > 0) ? 1u : 0u);
+          for (int u = 0; u < GS; ++u) {
+            if (u >= cnt) break;
+            const int dl = int((inf >> (8 + 5 * u)) & 31u);
+#pragma unroll
+            for (int sl = 0; sl < SLABS; ++sl)
+              tc::mma_i8(acc_t, tc::sdesc(tc::smem_u32(a + (u * SLABS + sl) * ASLAB)),
+                         tc::sdesc(tc::smem_u32(sB + (dl * SLABS + sl) * BSLAB)), IDESC32,
+                         ((inf & SI_ACC) || u > 0 || sl > 0) ? 1u : 0u);
+          }
         }
         tc::commit(&empty[st]);
         if (inf & SI_LAST) tc::commit(&tdone[b]);
@@ -400,26 +414,37 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
     auto bar_gather = [&]() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
     uint32_t g = 0;   // stage counter (uniform across the gather threads)
     int npend = 0;    // stages g - npend .. g - 1 issued by this thread, not yet arrived
-    auto issue_stage = [&](uint32_t inf, const int8_t* s0p, const int8_t* s1p, bool present) {
+    uint32_t zb = 0;  // bit GS st + u: this thread's row of sub-slot u of stage st holds zeros
+    uint8_t* a = sA;  // the open stage
+    auto stage_begin = [&]() {
       const uint32_t st = g % NS;
       if (g >= uint32_t(NS)) tc::mbar_wait(&empty[st], ((g / NS) - 1u) & 1u);
-      uint8_t* a = sA + st * SS * ASLAB;
+      a = sA + st * SS * ASLAB;
+    };
+    // sub-slot u of the open stage: the neighbour row (SLABS slabs), or zeros
+    auto put = [&](int u, const int8_t* s0p, const int8_t* s1p, bool present) {
+      uint8_t* au = a + u * SLABS * ASLAB;
+      const uint32_t zbit = 1u << ((g % NS) * GS + uint32_t(u));
       if (present) {
-        cp16(a + tc::kmaj_off(t, 0), s0p);
-        cp16(a + tc::kmaj_off(t, 16), s0p + 16);
-        if (SLABS == 2 || (inf & SI_PROJ)) {
-          cp16(a + ASLAB + tc::kmaj_off(t, 0), s1p);
-          cp16(a + ASLAB + tc::kmaj_off(t, 16), s1p + 16);
+        cp16(au + tc::kmaj_off(t, 0), s0p);
+        cp16(au + tc::kmaj_off(t, 16), s0p + 16);
+        if (SLABS == 2) {
+          cp16(au + ASLAB + tc::kmaj_off(t, 0), s1p);
+          cp16(au + ASLAB + tc::kmaj_off(t, 16), s1p + 16);
         }
-      } else {
+        zb &= ~zbit;
+      } else if (!(zb & zbit)) {  // an absent neighbour: zero the row once, keep it
         const uint4 z = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
         for (int sl = 0; sl < SLABS; ++sl) {
-          *reinterpret_cast<uint4*>(a + sl * ASLAB + tc::kmaj_off(t, 0)) = z;
-          *reinterpret_cast<uint4*>(a + sl * ASLAB + tc::kmaj_off(t, 16)) = z;
+          *reinterpret_cast<uint4*>(au + sl * ASLAB + tc::kmaj_off(t, 0)) = z;
+          *reinterpret_cast<uint4*>(au + sl * ASLAB + tc::kmaj_off(t, 16)) = z;
         }
+        zb |= zbit;
       }
-      if (t == 0) info[st] = inf;
+    };
+    auto stage_end = [&](uint32_t inf) {
+      if (t == 0) info[g % NS] = inf;
       cp_commit();
       ++npend;
       if (npend == NS - 1) {  // the oldest stage's copies have landed: hand it to the MMA warp
@@ -457,29 +482,50 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
       if (lane == 0) atomicOr(omask, my);
       bar_gather();
       const uint32_t mask = *omask;
-      const int cnt = __popc(mask) + (SKIP == 2 ? 1 : 0);
-      if (cnt == 0) {  // no neighbour anywhere in the tile: one zero stage (accumulator = 0)
-        issue_stage((13u << 8) | SI_LAST | bufbit, nullptr, nullptr, false);
+      const int noff = __popc(mask);
+      if (noff == 0 && SKIP != 2) {  // no neighbour anywhere in the tile: one zero stage (accumulator = 0)
+        stage_begin();
+        put(0, nullptr, nullptr, false);
+        stage_end((13u << 8) | (1u << 5) | SI_LAST | bufbit);
       } else {
-        int k = 0;
-        for (uint32_t m = mask; m; m &= m - 1, ++k) {
-          const int dl = __ffs(m) - 1;
-          int32_t j = int32_t(n);
+        // offsets in increasing order, GS per stage, with static register indices (the
+        // mask is uniform over the tile, so the branches are too)
+        int k = 0, u = 0;
+        uint32_t dls = 0;
 #pragma unroll
-          for (int d2 = 0; d2 < 27; ++d2)
-            if (d2 == dl) j = nb[d2];
-          const uint32_t inf = (uint32_t(dl) << 8) | bufbit | (k > 0 ? SI_ACC : 0u) | (k == cnt - 1 ? SI_LAST : 0u);
-          issue_stage(inf, in0 + size_t(j) * 32, SLABS == 2 ? in1 + size_t(j) * 32 : nullptr, j != int32_t(n));
+        for (int dl = 0; dl < 27; ++dl) {
+          if (!(mask >> dl & 1u)) continue;
+          if (u == 0) stage_begin();
+          const int32_t j = nb[dl];
+          put(u, in0 + size_t(j) * 32, SLABS == 2 ? in1 + size_t(j) * 32 : nullptr, j != int32_t(n));
+          dls |= uint32_t(dl) << (8 + 5 * u);
+          ++u;
+          ++k;
+          if (u == GS || k == noff) {
+            const bool first = k == u;
+            stage_end(dls | (uint32_t(u) << 5) | bufbit | (first ? 0u : SI_ACC) |
+                      (k == noff && SKIP != 2 ? SI_LAST : 0u));
+            u = 0;
+            dls = 0;
+          }
         }
         if constexpr (SKIP == 2) {  // 1x1 projection of the concat, own row
           const uint32_t ii = valid ? i : n;
-          issue_stage(SI_PROJ | SI_LAST | bufbit | (k > 0 ? SI_ACC : 0u), skip0 + size_t(ii) * 32,
-                      skip1 + size_t(ii) * 32, true);
+          stage_begin();
+          cp16(a + tc::kmaj_off(t, 0), skip0 + size_t(ii) * 32);
+          cp16(a + tc::kmaj_off(t, 16), skip0 + size_t(ii) * 32 + 16);
+          cp16(a + ASLAB + tc::kmaj_off(t, 0), skip1 + size_t(ii) * 32);
+          cp16(a + ASLAB + tc::kmaj_off(t, 16), skip1 + size_t(ii) * 32 + 16);
+#pragma unroll
+          for (int uu = 0; uu < GS; ++uu)  // the projection overwrote sub-slots 0 .. 2 / SLABS - 1
+            if (uu * SLABS < 2) zb &= ~(1u << ((g % NS) * GS + uint32_t(uu)));
+          stage_end(SI_PROJ | SI_LAST | bufbit | (noff > 0 ? SI_ACC : 0u));
         }
       }
     }
     // tell the MMA warp to stop, and hand over everything still pending
-    issue_stage(SI_END, nullptr, nullptr, false);
+    stage_begin();
+    stage_end(SI_END);
     drain();
   } else {  // ---- epilogue warps (5..8): TMEM lane quarter warp % 4 ----
     const int r = 32 * (warp & 3) + lane;
@@ -549,9 +595,9 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
 template <int SLABS, int SKIP>
 void launch_ws(pcc_ctx c, const int8_t* in0, const int8_t* in1, uint32_t n, const int32_t* nbr, const DConv& L,
                const int8_t* s0, const int8_t* s1, int32_t k_s, const int8_t* P, int8_t* out) {
-  constexpr int SS = (SKIP == 2) ? 2 : SLABS;
-  constexpr int smem = 27 * SLABS * 1024 + (SKIP == 2 ? 2048 : 0) + WS_NS * SS * 4096 + (2 * WS_NS + 4) * 8 +
-                       WS_NS * 4 + 16 + 128 + 64;
+  constexpr int SS = ws_slabs<SLABS, SKIP>(), NS = WsCfg<SLABS>::NS;
+  constexpr int smem = 27 * SLABS * 1024 + (SKIP == 2 ? 2048 : 0) + NS * SS * 4096 + (2 * NS + 4) * 8 + NS * 4 + 16 +
+                       128 + 64;
   auto kern = k_conv3_ws<SLABS, SKIP>;
   PCC_SMEM_ATTR(kern, smem);
   const uint32_t ntiles = (n + 1 + CT - 1) / CT;
