@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
   if (warp == 0) tc::tmem_alloc<64>(thold);  // two 32-column accumulators
   if (t == 0) {
     for (int i = 0; i < NS; ++i) {
-      tc::mbar_init(&full[i], CT);
+      tc::mbar_init(&full[i], CT + 1);  // each gather thread's copies landed + thread 0's info
       tc::mbar_init(&empty[i], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
       for (uint32_t g = 0;; ++g) {
         const uint32_t st = g % NS;
         tc::mbar_wait(&full[st], (g / NS) & 1u);
+        tc::fence_async_smem();  // the gathered rows (written by cp.async) to the async proxy
         tc::fence_after();
         const uint32_t inf = info[st];
         if (inf & SI_END) break;
@@ -413,7 +414,6 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
   } else if (warp < 4) {  // ---- gather warps: thread t = row t of the tile ----
     auto bar_gather = [&]() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
     uint32_t g = 0;   // stage counter (uniform across the gather threads)
-    int npend = 0;    // stages g - npend .. g - 1 issued by this thread, not yet arrived
     uint32_t zb = 0;  // bit GS st + u: this thread's row of sub-slot u of stage st holds zeros
     uint8_t* a = sA;  // the open stage
     auto stage_begin = [&]() {
@@ -443,26 +443,20 @@ __global__ void __launch_bounds__(WS_NT) k_conv3_ws(const int8_t* __restrict__ i
         zb |= zbit;
       }
     };
+    // the stage is handed over without waiting: each thread's arrival on FULL fires when its
+    // copies have landed (cp.async.mbarrier.arrive.noinc), so all NS stages can be in flight;
+    // thread 0 publishes the stage info with one more (release) arrival
     auto stage_end = [&](uint32_t inf) {
-      if (t == 0) info[g % NS] = inf;
-      cp_commit();
-      ++npend;
-      if (npend == NS - 1) {  // the oldest stage's copies have landed: hand it to the MMA warp
-        cp_wait<NS - 2>();
-        tc::fence_async_smem();
-        tc::mbar_arrive(&full[(g + 1u - uint32_t(npend)) % NS]);
-        --npend;
+      const uint32_t st = g % NS;
+      tc::fence_async_smem();  // this thread's zero rows
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&full[st])) : "memory");
+      if (t == 0) {
+        info[st] = inf;
+        tc::mbar_arrive(&full[st]);
       }
       ++g;
     };
-    auto drain = [&]() {
-      cp_wait<0>();
-      tc::fence_async_smem();
-#pragma unroll
-      for (int k = 0; k < NS - 1; ++k)
-        if (k < npend) tc::mbar_arrive(&full[(g - uint32_t(npend) + uint32_t(k)) % NS]);
-      npend = 0;
-    };
+    auto drain = [&]() {};
     uint32_t it = 0;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const uint32_t i = tile * CT + uint32_t(t);
