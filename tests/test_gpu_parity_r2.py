@@ -268,3 +268,42 @@ def test_bench_launch_configuration_all_frames(pcc):
     for i in range(nf):
         assert np.array_equal(dec[no[i]:no[i + 1]], morton_sorted_unique(frames[i], 12)), i
     codec.close()
+
+
+# ---------------------------------------------------------------------------------------
+# host-buffer calls (the e2e path)
+# ---------------------------------------------------------------------------------------
+
+def test_host_buffer_api(pcc, ctx):
+    """pcc_encode_batch_host / pcc_decode_batch_host (pinned host buffers in and out) on 70
+    cfg2 frames give the device-buffer batch call's bytes and decodes, and sampled frames
+    equal the oracle."""
+    mobj = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18)
+    mb = mobj.to_bytes()
+    om = O.Model(mb)
+    frames = I.make_frames(I.CFG2, 70, 0)
+    L = I.CFG2.bit_depth
+    m = pcc.pcc_model_load(mb, 0)
+    try:
+        want, oo_dev = gpu_encode(pcc, ctx, m, frames, L)
+        offs = np.cumsum([0] + [len(f) for f in frames]).tolist()
+        h_xyz = torch.from_numpy(np.concatenate(frames).astype(np.int32)).pin_memory()
+        cap = sum(pcc.pcc_encode_bound(len(f), L) + 4 for f in frames)
+        h_bs = torch.empty(cap, dtype=torch.uint8).pin_memory()
+        oo = pcc.pcc_encode_batch_host(ctx, m, h_xyz, offs, L, h_bs, cap)
+        blob = h_bs[:oo[-1]].numpy().tobytes()
+        got = [blob[oo[i]:oo[i + 1]] for i in range(len(frames))]
+        assert got == want
+        for i in (0, 63, 64, 69):
+            assert got[i] == O.encode(om, frames[i], L), i
+        n = offs[-1]
+        h_out = torch.empty((n, 3), dtype=torch.int32).pin_memory()
+        no = pcc.pcc_decode_batch_host(ctx, m, h_bs, list(oo), h_out, n)
+        dec = gpu_decode(pcc, ctx, m, want, n)
+        xyz = h_out[:no[-1]].numpy()
+        for i in range(len(frames)):
+            assert np.array_equal(xyz[no[i]:no[i + 1]], dec[i]), i
+        for i in (0, 64, 69):
+            assert np.array_equal(dec[i], morton_sorted_unique(frames[i], L)), i
+    finally:
+        pcc.pcc_model_destroy(m)
