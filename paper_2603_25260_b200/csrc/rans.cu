@@ -33,10 +33,23 @@ __global__ void __launch_bounds__(128) k_rans_enc(const EncSeg* __restrict__ seg
   uint32_t cnt = 0;
   uint16_t* end = words + sg.node + n;
   const unsigned above = ~((2u << gl) - 1u) & 0xffu;  // lanes of the group with a higher index
+  // the (cum, freq) words do not depend on the state: load them EP steps ahead in a
+  // register ring so the serial state chain never waits on memory
+  constexpr int EP = 8;
+  auto ldcf = [&](uint32_t s) -> uint32_t {
+    const uint32_t j = s * uint32_t(K) + uint32_t(gl);
+    return (s < steps && gl < K && j < n) ? __ldg(cf + sg.node + j) : 0u;
+  };
+  uint32_t ring[EP];
+#pragma unroll
+  for (int e = 0; e < EP; ++e) ring[e] = steps_max > uint32_t(e) ? ldcf(steps_max - 1u - uint32_t(e)) : 0u;
   for (uint32_t s = steps_max; s-- > 0;) {
     const uint32_t j = s * uint32_t(K) + uint32_t(gl);
     const bool act = s < steps && gl < K && j < n;
-    const uint32_t v = act ? cf[sg.node + j] : 0u;
+    const uint32_t v = ring[0];
+#pragma unroll
+    for (int e = 0; e < EP - 1; ++e) ring[e] = ring[e + 1];
+    ring[EP - 1] = s >= uint32_t(EP) ? ldcf(s - uint32_t(EP)) : 0u;
     const uint32_t c = v & 0xffffu, f = v >> 16;
     const bool emit = act && x >= (f << 16);
     const unsigned m = (__ballot_sync(0xffffffffu, emit) >> gb) & 0xffu;
