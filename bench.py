@@ -359,53 +359,14 @@ class GpuRunner:
                     self.bs = torch.empty(self.cap, dtype=torch.uint8, device=runner.device)
                     self.out = torch.empty((self.n, 3), dtype=torch.int32, device=runner.device)
                 self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-                self.pipe = bool(runner.args.pipeline)
-                if self.pipe:  # decoder instance: own ctx + stream, the previous step's streams
-                    self.dstream = torch.cuda.Stream(runner.dev)
-                    self.dctx = pcc.pcc_ctx_create(runner.dev, self.dstream.cuda_stream)
-                    self.bs2 = torch.empty(self.cap, dtype=torch.uint8, device=runner.device)
-                    self.prev = None  # (buffer, offsets) encoded by the previous step
 
             def run(self, start_ev=None):
-                if self.pipe:
-                    return self.run_pipelined(start_ev)
                 if start_ev is not None:
                     self.stream.wait_event(start_ev)
                 self.oo = pcc.pcc_encode_batch(self.ctx, runner.model, self.xyz, self.offs, L, self.bs, self.cap)
                 self.ev[0].record(self.stream)
                 self.no = pcc.pcc_decode_batch(self.ctx, runner.model, self.bs, self.oo, self.out, self.n)
                 self.ev[1].record(self.stream)
-
-            def run_pipelined(self, start_ev=None):
-                """--pipeline: encode this step's frames while a second instance decodes the
-                streams the previous step encoded (the same frames): one step is still one
-                encode and one decode of every frame; the two halves overlap on the GPU."""
-                import threading as _th
-                if self.prev is None:  # first call: produce the streams the next step decodes
-                    self.stream.wait_event(start_ev) if start_ev is not None else None
-                    self.oo = pcc.pcc_encode_batch(self.ctx, runner.model, self.xyz, self.offs, L, self.bs, self.cap)
-                    self.prev = (self.bs, self.oo)
-                    self.ev[0].record(self.stream)
-                    self.no = pcc.pcc_decode_batch(self.ctx, runner.model, self.bs, self.oo, self.out, self.n)
-                    self.ev[1].record(self.stream)
-                    self.dstream.wait_stream(self.stream)
-                    return
-                pbuf, poo = self.prev
-                cur = self.bs2 if pbuf is self.bs else self.bs
-                if start_ev is not None:
-                    self.stream.wait_event(start_ev)
-                    self.dstream.wait_event(start_ev)
-
-                def dec():
-                    self.no = pcc.pcc_decode_batch(self.dctx, runner.model, pbuf, poo, self.out, self.n)
-                    self.ev[1].record(self.dstream)
-                t = _th.Thread(target=dec)
-                t.start()
-                self.oo = pcc.pcc_encode_batch(self.ctx, runner.model, self.xyz, self.offs, L, cur, self.cap)
-                self.ev[0].record(self.stream)
-                t.join()
-                self.prev = (cur, self.oo)
-                self.bs = cur  # parity reads the last encode (identical to the decoded streams)
 
         return Lane()
 
@@ -424,7 +385,6 @@ class GpuRunner:
             t_.join()
         end = torch.cuda.Event(enable_timing=True)
         for ln in self.lanes:
-            self.main.wait_event(ln.ev[0])
             self.main.wait_event(ln.ev[1])
         end.record(self.main)
         return start, end
@@ -470,8 +430,7 @@ class GpuRunner:
             torch.cuda.synchronize(self.dev)  # the lanes' events are reused next step
             tot.append(start.elapsed_time(end))
             enc.append(max(start.elapsed_time(ln.ev[0]) for ln in self.lanes))
-            dec.append(max((start.elapsed_time(ln.ev[1]) if ln.pipe else ln.ev[0].elapsed_time(ln.ev[1]))
-                           for ln in self.lanes))
+            dec.append(max(ln.ev[0].elapsed_time(ln.ev[1]) for ln in self.lanes))
         return tot, enc, dec
 
     def launches_per_step(self):
@@ -757,8 +716,6 @@ def main(argv=None):
                     help="frames per GPU per step (default: 1024 = 4 codec lanes x 256 frames for "
                          "L <= 13, 256 for the deeper configs, whose per-lane arenas are larger)")
     ap.add_argument("--streams", type=int, default=4, help="concurrent codec lanes (ctx + stream) per GPU")
-    ap.add_argument("--pipeline", action="store_true",
-                    help="each lane decodes the previous step's streams while encoding this step's frames")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
