@@ -56,18 +56,35 @@ __global__ void __launch_bounds__(MD_T) k_morton_dedup(const int32_t* __restrict
   const uint64_t fb = B > 1 ? uint64_t(f) << (3 * L) : 0ull;
   uint64_t kv[MD_V];
   uint32_t keepm = 0, woff[MD_V];
+  // all MD_V points' coordinates first (independent loads in flight together), then the
+  // keys; the previous point of a lane's point is the lower lane's (a shuffle), lane 0
+  // loads it
+  int32_t px[MD_V], py[MD_V], pz[MD_V], qx[MD_V], qy[MD_V], qz[MD_V];
+#pragma unroll
+  for (int v = 0; v < MD_V; ++v) {
+    const uint32_t i = c0 + uint32_t(v) * MD_T + threadIdx.x;
+    px[v] = py[v] = pz[v] = 0;
+    qx[v] = qy[v] = qz[v] = -1;
+    if (i < nf) {
+      const int32_t* p = xyz + 3 * (a + i);
+      px[v] = p[0], py[v] = p[1], pz[v] = p[2];
+      if (lane == 0 && i > 0) qx[v] = p[-3], qy[v] = p[-2], qz[v] = p[-1];
+    }
+  }
 #pragma unroll
   for (int v = 0; v < MD_V; ++v) {
     const uint32_t i = c0 + uint32_t(v) * MD_T + threadIdx.x;  // frame-local point index
+    const int32_t x = px[v], y = py[v], z = pz[v];
+    const int32_t ux = __shfl_up_sync(0xffffffffu, x, 1), uy = __shfl_up_sync(0xffffffffu, y, 1),
+                  uz = __shfl_up_sync(0xffffffffu, z, 1);
+    const int32_t prx = lane ? ux : qx[v], pry = lane ? uy : qy[v], prz = lane ? uz : qz[v];
     bool keep = false;
     kv[v] = 0;
     if (i < nf) {
-      const int32_t* p = xyz + 3 * (a + i);
-      const int32_t x = p[0], y = p[1], z = p[2];
       if (x < 0 || y < 0 || z < 0 || x >= lim || y >= lim || z >= lim) {
         atomicOr(err, EF_RANGE);
       } else {
-        keep = i == 0 || p[-3] != x || p[-2] != y || p[-1] != z;
+        keep = i == 0 || prx != x || pry != y || prz != z;
         kv[v] = fb | spread3(uint32_t(x)) << 2 | spread3(uint32_t(y)) << 1 | spread3(uint32_t(z));
       }
     }
