@@ -55,7 +55,8 @@ struct Smem4 {
   static constexpr int MBAR = F + 4096 * NG;   // NG mbarriers
   static constexpr int THOLD = MBAR + 8 * NG;
   static constexpr int LUT = MBAR + 128;       // [1025][32] u32, 32 interleaved copies
-  static constexpr int END = LUT + 1025 * 32 * 4;
+  static constexpr int CS = LUT + 1025 * 32 * 4;  // decoder: block sums [16][NG * 128] u32
+  static constexpr int END = CS + 16 * NG * 128 * 4;
 };
 
 template <int C, int H, int MODE, bool SAT, int NG>
@@ -255,12 +256,11 @@ __global__ void __launch_bounds__(NG * 128, 1) k_head4_tc(const int8_t* __restri
     // ---- pass 2: e_i = LUT[(mu - l_i) >> 2], 16-symbol block sums, the encoder's prefix mass.
     // Half 1 first (its logits are still in TMEM), then half 0 again.
     uint32_t Sacc = 0, pre = 0, es = 0;
-    uint32_t c0s[8], c1s[8];  // decoder: the 16-symbol block sums of half 0 / half 1
+    uint32_t* scs = reinterpret_cast<uint32_t*>(sm + S::CS) + tid;  // decoder: block b's sum at scs[b * NT1]
 #pragma unroll 1
     for (int hh = 0; hh < 2; ++hh) {
       const int h = 1 - hh;
       if (hh == 1) mma2(adesc, w2d0, kdesc, b2d0, IDESC_Z);
-      uint32_t hb[8];  // decoder: the half's block sums, shifted in (static register indices)
 #pragma unroll 1
       for (int ch4 = 0; ch4 < 4; ++ch4) {
         const int ch = 4 * h + ch4;
@@ -303,20 +303,9 @@ __global__ void __launch_bounds__(NG * 128, 1) k_head4_tc(const int8_t* __restri
               }
             }
           } else {
-#pragma unroll
-            for (int i = 0; i < 7; ++i) hb[i] = hb[i + 1];
-            hb[7] = s16;
+            scs[(2 * ch + hf) * NT1] = s16;
           }
           Sacc += s16;  // <= 255 * 2^24 < 2^32
-        }
-      }
-      if constexpr (MODE == 1) {
-        if (h == 1) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) c1s[i] = hb[i];
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) c0s[i] = hb[i];
         }
       }
     }
@@ -333,7 +322,7 @@ __global__ void __launch_bounds__(NG * 128, 1) k_head4_tc(const int8_t* __restri
       uint32_t Eb[16];
       Eb[0] = 0u;
 #pragma unroll
-      for (int k = 1; k < 16; ++k) Eb[k] = Eb[k - 1] + (k <= 8 ? c0s[k - 1] : c1s[k - 9]);
+      for (int k = 1; k < 16; ++k) Eb[k] = Eb[k - 1] + scs[(k - 1) * NT1];
       uint4* dst = reinterpret_cast<uint4*>(rows + size_t(row) * DROW_BYTES);
       const uint32_t inv32 = uint32_t((65281ull << 32) / uint64_t(Ssum));
       dst[0] = make_uint4(Ssum, inv32, uint32_t(mu), Eb[1]);
