@@ -55,7 +55,7 @@ struct Smem4 {
   static constexpr int MBAR = F + 4096 * NG;   // NG mbarriers
   static constexpr int THOLD = MBAR + 8 * NG;
   static constexpr int LUT = MBAR + 128;       // [1025][32] u32, 32 interleaved copies
-  static constexpr int CS = LUT + 1025 * 32 * 4;  // decoder: block sums [16][NG * 128] u32
+  static constexpr int CS = LUT + 1025 * 32 * 4;  // [16][NG * 128] u32: decoder block sums / encoder's symbol block
   static constexpr int END = CS + 16 * NG * 128 * 4;
 };
 
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(NG * 128, 1) k_head4_tc(const int8_t* __restri
     // ---- pass 2: e_i = LUT[(mu - l_i) >> 2], 16-symbol block sums, the encoder's prefix mass.
     // Half 1 first (its logits are still in TMEM), then half 0 again.
     uint32_t Sacc = 0, pre = 0, es = 0;
-    uint32_t* scs = reinterpret_cast<uint32_t*>(sm + S::CS) + tid;  // decoder: block b's sum at scs[b * NT1]
+    uint32_t* scs = reinterpret_cast<uint32_t*>(sm + S::CS) + tid;  // word k of this thread at scs[k * NT1]
 #pragma unroll 1
     for (int hh = 0; hh < 2; ++hh) {
       const int h = 1 - hh;
@@ -292,15 +292,14 @@ __global__ void __launch_bounds__(NG * 128, 1) k_head4_tc(const int8_t* __restri
 #pragma unroll
           for (int k = 0; k < 16; ++k) s16 += v[16 * hf + k];
           if constexpr (MODE == 0) {
+            // whole blocks below the symbol add to its prefix mass; the symbol's own block
+            // is parked in shared memory and finished after the pass (16 stores instead of
+            // a 16-step compare-select chain under a divergent branch)
             const int i0 = 32 * ch + 16 * hf;
-            if (sym >= i0 + 16) {
-              pre += s16;
-            } else if (sym >= i0) {
+            pre += sym >= i0 + 16 ? s16 : 0u;
+            if (sym >= i0 && sym < i0 + 16) {
 #pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                pre += (i0 + k < sym) ? v[16 * hf + k] : 0u;
-                es = (i0 + k == sym) ? v[16 * hf + k] : es;
-              }
+              for (int k = 0; k < 16; ++k) scs[k * NT1] = v[16 * hf + k];
             }
           } else {
             scs[(2 * ch + hf) * NT1] = s16;
@@ -311,6 +310,15 @@ __global__ void __launch_bounds__(NG * 128, 1) k_head4_tc(const int8_t* __restri
     }
     const uint32_t Ssum = Sacc;
     if constexpr (MODE == 0) {
+      {  // the symbol's block: prefix within it and the symbol's own e
+        const int m = sym & 15;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const uint32_t e = scs[k * NT1];
+          pre += k < m ? e : 0u;
+          es = k == m ? e : es;
+        }
+      }
       if (valid) {  // (cum, freq) = (C_sym, C_{sym+1} - C_sym), reading Q21
         const float rS = 65281.0f / float(Ssum);
         const uint32_t c0 = uint32_t(sym) + qdiv(pre, Ssum, rS);
