@@ -377,24 +377,52 @@ __global__ void k_popc(const uint8_t* __restrict__ X, uint32_t n, uint32_t* __re
 }
 
 // cap: room left in the node arrays (a corrupt stream can decode more children than any
-// valid one; those are dropped and flagged instead of written out of bounds)
+// valid one; those are dropped and flagged instead of written out of bounds).  A warp
+// expands 32 consecutive parents: their children are one contiguous run of the next
+// depth, written lane-strided (coalesced 8- and 4-byte stores); child e of the run belongs
+// to the lane whose exclusive child prefix is the largest <= e (binary search over the
+// lanes by shuffles), and is that lane's (e - prefix)-th set occupancy bit (__fns).
 __global__ void k_expand(const uint64_t* __restrict__ key_d, const uint8_t* __restrict__ X, const uint32_t* __restrict__ cs,
                          uint32_t n, uint64_t* __restrict__ key_c, uint32_t* __restrict__ par_c, uint64_t cap,
                          uint32_t* __restrict__ err) {
-  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  uint32_t x = X[p], j = cs[p];
-  const uint64_t k = key_d[p] << 3;
-  for (int c = 0; c < 8; ++c)
-    if ((x >> c) & 1u) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const uint32_t p0 = p - uint32_t(lane);
+  if (p0 >= n) return;  // whole warp
+  const bool ok = p < n;
+  const uint32_t x = ok ? uint32_t(X[p]) : 0u;
+  const uint64_t k = ok ? key_d[p] << 3 : 0ull;
+  const uint32_t j0 = cs[p0];
+  uint32_t incl = __popc(x);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const uint32_t excl = incl - __popc(x);
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  for (uint32_t e0 = 0; e0 < total; e0 += 32) {
+    const uint32_t e = e0 + uint32_t(lane);
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const uint32_t ex = __shfl_sync(0xffffffffu, excl, lo + step);
+      if (ex <= e) lo += step;
+    }
+    const uint32_t xo = __shfl_sync(0xffffffffu, x, lo);
+    const uint32_t eo = __shfl_sync(0xffffffffu, excl, lo);
+    const uint64_t ko = __shfl_sync(0xffffffffu, k, lo);
+    if (e < total) {
+      const uint32_t c = __fns(xo, 0, int(e - eo) + 1);  // the (e - eo)-th set bit (from 0)
+      const uint64_t j = uint64_t(j0) + e;
       if (j < cap) {
-        key_c[j] = k | uint64_t(c);
-        par_c[j] = p;
+        key_c[j] = ko | uint64_t(c);
+        par_c[j] = p0 + uint32_t(lo);
       } else if (err) {
         atomicOr(err, EF_CORRUPT);
       }
-      ++j;
     }
+  }
 }
 
 __global__ void k_foff_next(const uint32_t* __restrict__ cs, const uint32_t* __restrict__ foff_d, int B,
