@@ -1014,7 +1014,7 @@ void decode_batch(pcc_ctx c, pcc_model m, const uint8_t* d_bs, const size_t* bs_
   // 3. level-serial neural decoding (Eq.2)
   Net net{c, m, L, R, L - 1 - m->n_deep, C, o};
   // pinned staging for every level's segment list (upper bound: per level, one segment
-  // per frame plus one per 16384 nodes)
+  // per frame plus one per SEG_SYMS nodes)
   const size_t seg_ring_cap = size_t(L - R) * ((size_t(B) + NLtot / SEG_SYMS + 2) * sizeof(DecSeg) + 256);
   uint8_t* seg_ring = static_cast<uint8_t*>(pinned_ring(c, seg_ring_cap));
   size_t seg_ring_used = 0;
