@@ -275,9 +275,9 @@ def test_bench_launch_configuration_all_frames(pcc):
 # ---------------------------------------------------------------------------------------
 
 def test_host_buffer_api(pcc, ctx):
-    """pcc_encode_batch_host / pcc_decode_batch_host (pinned host buffers in and out) on 70
-    cfg2 frames give the device-buffer batch call's bytes and decodes, and sampled frames
-    equal the oracle."""
+    """pcc_encode_batch_host / pcc_decode_batch_host on 70 cfg2 frames, pinned and pageable
+    host buffers: the device-buffer batch call's bytes and decodes; sampled frames equal the
+    oracle."""
     mobj = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18)
     mb = mobj.to_bytes()
     om = O.Model(mb)
@@ -305,5 +305,16 @@ def test_host_buffer_api(pcc, ctx):
             assert np.array_equal(xyz[no[i]:no[i + 1]], dec[i]), i
         for i in (0, 64, 69):
             assert np.array_equal(dec[i], morton_sorted_unique(frames[i], L)), i
+        # pageable host buffers (numpy)
+        sub = frames[:5]
+        soffs = np.cumsum([0] + [len(f) for f in sub]).tolist()
+        p_xyz = np.ascontiguousarray(np.concatenate(sub).astype(np.int32))
+        p_bs = np.zeros(sum(pcc.pcc_encode_bound(len(f), L) + 4 for f in sub), np.uint8)
+        poo = pcc.pcc_encode_batch_host(ctx, m, p_xyz, soffs, L, p_bs, p_bs.size)
+        assert [p_bs[poo[i]:poo[i + 1]].tobytes() for i in range(5)] == want[:5]
+        p_out = np.zeros((soffs[-1], 3), np.int32)
+        pno = pcc.pcc_decode_batch_host(ctx, m, p_bs, list(poo), p_out, soffs[-1])
+        for i in range(5):
+            assert np.array_equal(p_out[pno[i]:pno[i + 1]], dec[i]), i
     finally:
         pcc.pcc_model_destroy(m)
