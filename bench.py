@@ -72,10 +72,15 @@ def workload(args):
 
 
 def default_batch(name: str) -> int:
-    """Frames per GPU per step when --batch is not given: 1024 (4 lanes x 256 frames) where
-    a lane's arena fits comfortably (L <= 13), 256 for the deeper trees (L >= 14, cfg3)."""
-    deep = name == "cfg3" or (name.startswith("cfg2_L") and int(name[6:]) >= 14)
-    return 256 if deep else 1024
+    """Frames per GPU per step when --batch is not given: 2048 (4 lanes x 512 frames per
+    codec launch) for the L <= 12 workloads (measured 31.0k against 28.3k frames/s at 4 x
+    256: the level-serial decoder and the per-launch fixed costs amortise over more frames),
+    1024 at L = 13, 256 for the deeper trees (L >= 14, cfg3), whose arenas are larger."""
+    if name == "cfg3" or (name.startswith("cfg2_L") and int(name[6:]) >= 14):
+        return 256
+    if name == "cfg2_L13":
+        return 1024
+    return 2048
 
 
 def model_bytes(args, C):
@@ -713,8 +718,8 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=None,
-                    help="frames per GPU per step (default: 1024 = 4 codec lanes x 256 frames for "
-                         "L <= 13, 256 for the deeper configs, whose per-lane arenas are larger)")
+                    help="frames per GPU per step (default: 2048 = 4 codec lanes x 512 frames for "
+                         "L <= 12, 1024 at L = 13, 256 for the deeper configs)")
     ap.add_argument("--streams", type=int, default=4, help="concurrent codec lanes (ctx + stream) per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

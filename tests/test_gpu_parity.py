@@ -487,20 +487,20 @@ def test_alternate_kernels_bit_exact(pcc, env):
 
 
 def test_bench_launch_configuration_sampled(pcc):
-    """BASELINE.json full size in the launch configuration bench.py times (cfg2, 256 frames
-    per codec launch = one of its 4 lanes at the default batch of 1024, C = H = 32): sampled
+    """BASELINE.json full size in the launch configuration bench.py times (cfg2, 512 frames
+    per codec launch = one of its 4 lanes at the default batch of 2048, C = H = 32): sampled
     bitstreams byte-identical to the oracle, and every frame of the batch decodes to its
     unique voxels in Morton order."""
     from paper_2603_25260_b200.pcc import Codec
     mb, om = model_pair(32)
-    nf = 256
+    nf = 512
     frames = I.make_frames(I.CFG2, nf, first=0, scene_seed=1)
     offs = np.cumsum([0] + [len(f) for f in frames]).tolist()
     codec = Codec(mb, 0)
     out, oo = codec.encode_frames(dev(np.concatenate(frames)), offs, 12)
     xyz, no = codec.decode_frames(out, oo, offs[-1])
     host = out[:oo[-1]].cpu().numpy().tobytes()
-    for i in (0, 137, nf - 1):
+    for i in (0, 137, 300, nf - 1):
         assert host[oo[i]:oo[i + 1]] == O.encode(om, frames[i], 12), i
     dec = xyz[:no[-1]].cpu().numpy()
     for i in range(nf):

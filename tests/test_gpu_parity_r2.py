@@ -247,13 +247,13 @@ def test_decoder_rows_c32(pcc, ctx):
 # ---------------------------------------------------------------------------------------
 
 def test_bench_launch_configuration_all_frames(pcc):
-    """cfg2 at full size, 256 frames per codec launch (one of bench.py's 4 lanes at its
-    default batch of 1024), C = H = 32: EVERY frame's bitstream byte-identical to the
+    """cfg2 at full size, 512 frames per codec launch (one of bench.py's 4 lanes at its
+    default batch of 2048), C = H = 32: EVERY frame's bitstream byte-identical to the
     oracle (oracle encodes on all host cores), every frame decodes to its voxels."""
     from paper_2603_25260_b200.pcc import Codec
     mb = I.make_model(C=32, H=32, seed=1, min_depth=9, max_depth=18).to_bytes()
     om = O.Model(mb)
-    nf = 256
+    nf = 512
     frames = I.make_frames(I.CFG2, nf, first=0, scene_seed=1)
     offs = np.cumsum([0] + [len(f) for f in frames]).tolist()
     codec = Codec(mb, 0)

@@ -79,11 +79,12 @@ def test_sequence_shard_covers_every_frame_once():
 
 
 def test_default_batch_per_workload():
-    """bench defaults: 1024 frames per GPU (4 lanes x 256) up to L = 13, 256 for deeper trees."""
+    """bench defaults: 2048 frames per GPU (4 lanes x 512) up to L = 12, 1024 at L = 13, 256 for
+    deeper trees."""
     import bench
-    assert bench.default_batch("cfg2") == 1024 and bench.default_batch("cfg2_L13") == 1024
+    assert bench.default_batch("cfg2") == 2048 and bench.default_batch("cfg2_L13") == 1024
     assert bench.default_batch("cfg2_L14") == 256 and bench.default_batch("cfg3") == 256
-    assert bench.default_batch("cfg2_t3") == 1024
+    assert bench.default_batch("cfg2_t3") == 2048
 
 
 def test_bench_gpus2_spawns_two_gloo_ranks():

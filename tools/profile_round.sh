@@ -9,7 +9,7 @@ tail -c 300 gpurun_out/bench_default.log
 timeout -s KILL 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_reference.log 2>&1
 tail -c 300 gpurun_out/bench_reference.log
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/launches.csv python tools/step_once.py --batch 256 --steps 0 > gpurun_out/ncu_launches.log 2>&1
+  --log-file gpurun_out/launches.csv python tools/step_once.py --batch 512 --steps 0 > gpurun_out/ncu_launches.log 2>&1
 echo "launch list: $(wc -l < gpurun_out/launches.csv) lines"
 for k in "k_head4_tc<.int.32, .int.32, .int.1:head_dec" "k_head4_tc<.int.32, .int.32, .int.0:head_enc" \
          "k_rans_dec_t:rans_dec" "k_conv3_ws:conv" "k_up_tc:up" "k_down_tc:down" "k_rs_scatter:sort_scatter" \

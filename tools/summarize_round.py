@@ -3,7 +3,7 @@
 usage: python tools/summarize_round.py r01
   profiles/<tag>_bench.json         the default bench.py JSON line
   profiles/<tag>_bench_reference.json  the --impl reference line
-  profiles/<tag>_launches.txt       per-kernel totals / shares of one B=256 step (ncu launch list)
+  profiles/<tag>_launches.txt       per-kernel totals / shares of one B=512 step (ncu launch list)
   profiles/<tag>_ncu_full_<k>.txt   key metrics + DRAM bytes of the longest launch of kernel k
   profiles/traffic.json             DRAM bytes of those launches (bench.py roofline.traffic)
 """
@@ -42,7 +42,7 @@ def summarize(tag, name, path):
     kname = rows[1][hdr.index("Kernel Name")] if len(rows) > 1 else "?"
     raw = ncu_csv(path, "raw")
     rh, ru, rv = raw[0], raw[1], raw[2]
-    lines = [f"== {name}: longest launch of one B=256 step (ncu --set full --clock-control none)",
+    lines = [f"== {name}: longest launch of one B=512 step (ncu --set full --clock-control none)",
              f"   kernel: {kname[:110]}"]
     for k in KEYS:
         if k in m:
@@ -74,13 +74,13 @@ def main(tag):
                            capture_output=True, text=True).stdout
         open(os.path.join(PROF, f"{tag}_launches.txt"), "w").write(
             "# ncu --metrics gpu__time_duration.sum --clock-control none, one B=256 cfg2 step through one codec\n"
-            "# instance (tools/step_once.py --batch 256 --steps 0): cold-cache, serialised launches\n" + s)
+            "# instance (tools/step_once.py --batch 512 --steps 0): cold-cache, serialised launches\n" + s)
     traffic = {}
     for f in sorted(os.listdir(OUT)):
         if f.startswith("full_") and f.endswith(".ncu-rep"):
             name = f[5:-8]
             dram, dur = summarize(tag, name, os.path.join(OUT, f))
-            traffic[name] = {"dram_bytes_per_launch": dram, "launch": "longest launch of one B=256 step",
+            traffic[name] = {"dram_bytes_per_launch": dram, "launch": "longest launch of one B=512 step",
                              "duration": " ".join(dur) if dur else None, "source": f"profiles/{tag}_ncu_full_{name}.txt"}
     if traffic:  # keyed by workload (bench.py measured_traffic): these captures are cfg2 steps
         p = os.path.join(PROF, "traffic.json")
