@@ -172,9 +172,12 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def make_inputs(cfg, B: int, first: int):
+def make_inputs(cfg, B: int, first: int, world: int = 1):
+    """The rank's B synthetic frames (seeded per frame index), ray-cast on host threads."""
+    from concurrent.futures import ThreadPoolExecutor
     from paper_2603_25260_b200 import inputs as I
-    frames = I.make_frames(cfg, B, first=first, scene_seed=1)
+    with ThreadPoolExecutor(max_workers=max(1, (os.cpu_count() or 1) // max(1, world))) as ex:
+        frames = list(ex.map(lambda i: I.make_frame(cfg, first + i, scene_seed=1), range(B)))
     offs = np.cumsum([0] + [len(f) for f in frames]).tolist()
     return frames, offs
 
@@ -332,7 +335,7 @@ class GpuRunner:
             self.frames = [I.make_frame(cfg, i, scene_seed=1) for i in sequence_shard(rank, world)]
             self.offs = np.cumsum([0] + [len(f) for f in self.frames]).tolist()
         else:
-            self.frames, self.offs = make_inputs(cfg, args.batch, shard_frames(rank, world, args.batch)[0])
+            self.frames, self.offs = make_inputs(cfg, args.batch, shard_frames(rank, world, args.batch)[0], world)
         self.B = B = len(self.frames)
         self.S = S = max(1, min(args.streams, B))
         self.npts = self.offs[-1]
