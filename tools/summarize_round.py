@@ -73,7 +73,7 @@ def main(tag):
         s = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_summary.py"), p],
                            capture_output=True, text=True).stdout
         open(os.path.join(PROF, f"{tag}_launches.txt"), "w").write(
-            "# ncu --metrics gpu__time_duration.sum --clock-control none, one B=256 cfg2 step through one codec\n"
+            "# ncu --metrics gpu__time_duration.sum --clock-control none, one B=512 cfg2 step (one bench lane) through one codec\n"
             "# instance (tools/step_once.py --batch 512 --steps 0): cold-cache, serialised launches\n" + s)
     traffic = {}
     for f in sorted(os.listdir(OUT)):
