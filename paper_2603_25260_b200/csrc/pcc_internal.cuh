@@ -273,7 +273,8 @@ struct EncSeg {      // one rANS segment of the encoder
   uint32_t n;        // symbols
 };
 void rans_encode(pcc_ctx c, const EncSeg* d_segs, int nseg, const uint32_t* cf, uint16_t* words, uint32_t* seg_W,
-                 uint32_t* seg_state);
+                 uint32_t* seg_state,
+                 size_t nsym = 0);
 struct DecSeg {
   uint64_t byte;     // offset of the segment's level payload in the bitstream buffer
   uint32_t chunk;    // segment index within the level payload

@@ -621,10 +621,12 @@ __global__ void __launch_bounds__(32 * DEC_WPC) k_rans_dec_t(const DecSeg* __res
 }  // namespace
 
 void rans_encode(pcc_ctx c, const EncSeg* d_segs, int nseg, const uint32_t* cf, uint16_t* words, uint32_t* seg_W,
-                 uint32_t* seg_state) {
+                 uint32_t* seg_state,
+                 size_t nsym) {
   if (nseg == 0) return;
   const unsigned grid = unsigned((size_t(nseg) * MAX_LANES + 127) / 128);
-  Prof p(c, "rans_enc", 0);
+  // algorithmic bytes: the (cum, freq) word read and one 16-bit word written per symbol
+  Prof p(c, "rans_enc", nsym * (4 + 2));
   k_rans_enc<<<grid, 128, 0, c->stream>>>(d_segs, nseg, cf, words, seg_W, seg_state);
   launched(c);
 }

@@ -825,7 +825,9 @@ void encode_batch(pcc_ctx c, pcc_model m, const int32_t* d_xyz, const size_t* of
   uint16_t* words = buf<uint16_t>(c, "words", tot);
   uint32_t* seg_W = buf<uint32_t>(c, "seg_W", nseg);
   uint32_t* seg_state = buf<uint32_t>(c, "seg_state", size_t(nseg) * 32);
-  rans_encode(c, d_segs, nseg, cf, words, seg_W, seg_state);
+  size_t nsym = 0;
+  for (const EncSeg& sg : segs) nsym += sg.n;
+  rans_encode(c, d_segs, nseg, cf, words, seg_W, seg_state, nsym);
   uint32_t* sizes = buf<uint32_t>(c, "item_sizes", nit + 1);
   uint32_t* ioff = buf<uint32_t>(c, "item_off", nit + 1);
   uint64_t* d_nb = upload(c, "nb", o.nb);
